@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Benchmark: additive Vanka sweep on BASELINE config 2 (+ MG-FGMRES TTS).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): Taylor-Hood P2/P1 on the 256x256
+right-triangle grid, finest level of the 5-level hierarchy: N = 592,387 DoFs,
+J = 66,049 vertex-star patches (data/cfg2_pack.npz — the reference's assembled
+operators; setup is out of scope).  A *step* is one additive Vanka sweep
+(x = 0.5 * apply_additive(r)) over the whole level = two kernels (K4a patch
+solve, K4b patch-ordered accumulation).  value = patch-solves/s over all
+ranks; the MG-FGMRES(30) time-to-solution to 1e-8 is reported beside it.
+
+Multi-GPU: replicas only — every rank runs the same sweep
+workload on its own GPU, no collective on the data path; value = all ranks'
+patch-solves / max-over-ranks time ("scaling": "weak").
+
+--impl reference times the reference algorithm on the host cores: the
+CPU oracle (oracle/vanka_oracle.py — the reference's apply_additive
+restated, scipy getrs per patch, bit-exact with the reference) over a
+bounded sample of the same level's patches (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = "cfg2"
+METRIC = "Vanka sweep patch-solves/s (P2/P1 256x256 finest level, damping 0.5)"
+UNIT = "patch-solves/s"
+CPU_SAMPLE_PATCHES = 4096
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def _peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------
+# CPU reference arm / baseline (oracle = the reference algorithm restated)
+# ----------------------------------------------------------------------------
+
+def cpu_sweep_sample(pack, steps=3, warmup=1, sample=CPU_SAMPLE_PATCHES):
+    from oracle import vanka_oracle as O
+    lv = pack.fine
+    ps = O.build_patches(lv.mixed, lv.system.bc)
+    O.factor_patches(ps, lv.system, limit=sample)
+    n = lv.system.matrix.shape[0]
+    r = np.random.default_rng(1).uniform(-1.0, 1.0, n)
+    for _ in range(warmup):
+        O.apply_additive(ps, r, limit=sample)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        O.apply_additive(ps, r, limit=sample)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": sample / t, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"first {sample} of {ps.num_patches} patches of the {CONFIG} finest "
+                      f"level, scipy getrs per patch (reference apply_additive loop), "
+                      f"median of {steps}", "ms_per_step": t * 1e3}
+
+
+def run_reference(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    from paper_2409_14222_b200.pack import read_pack
+    pack = read_pack(os.path.join(ROOT, "data", f"{CONFIG}_pack.npz"))
+    cb = cpu_sweep_sample(pack, steps=args.steps, warmup=args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded residual)",
+            "config": {"workload": f"{CONFIG}: P2/P1 tri 256x256 finest level, one additive "
+                                   "sweep per step (bounded CPU sample)"},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2409_14222_b200 as V
+    from paper_2409_14222_b200 import _lib as L
+    from paper_2409_14222_b200.pack import read_pack
+    from paper_2409_14222_b200.solver import FgmresSolver, mg_rhs
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    pack = read_pack(os.path.join(ROOT, "data", f"{CONFIG}_pack.npz"))
+    t0 = time.perf_counter()
+    hier = V.hierarchy_from_pack(pack)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    fine = hier.fine
+    ps = fine.patches
+    ex = ps.export()
+    sizes = np.diff(ex["offsets"]).astype(np.int64)
+    J = int(ps.num_patches)
+    N = int(fine.n)
+    sum_s, sum_s2 = int(sizes.sum()), int((sizes ** 2).sum())
+    # algorithmic bytes
+    bytes_solve = 8 * sum_s2 + 4 * sum_s + 8 * sum_s + 8 * sum_s + 8 * N
+    bytes_sweep = 8 * sum_s2 + 12 * sum_s + 16 * N
+
+    r = torch.from_numpy(np.random.default_rng(1).uniform(-1.0, 1.0, N)).to(dev)
+    x = torch.empty_like(r)
+    stream = torch.cuda.current_stream()
+    sp = L.stream_ptr()
+    h = ps.handle
+
+    def step():
+        L.call("vk_patches_solve", h, L.ptr(r), sp)
+        L.call("vk_patches_accumulate", h, L.ptr(x), 0.5, L.VK_APPLY_XSET, sp)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K sweeps, per-kernel events on the launching stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for k in range(args.steps):
+            a, b, c = ev[k]
+            a.record(stream)
+            L.call("vk_patches_solve", h, L.ptr(r), sp)
+            b.record(stream)
+            L.call("vk_patches_accumulate", h, L.ptr(x), 0.5, L.VK_APPLY_XSET, sp)
+            c.record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+        # keep the GPU busy a little longer so the sampler sees load
+        extra_t0 = time.perf_counter()
+        while time.perf_counter() - extra_t0 < 1.0:
+            for _ in range(20):
+                step()
+            torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = start.elapsed_time(stop)
+    ms_solve = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    ms_gather = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    tmax = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_total = float(tmax.item())
+    ms_step = ms_total / args.steps
+    value = world * J * args.steps / (ms_total * 1e-3)
+
+    # ---- e2e through the public API: pinned host residual in, host out
+    r_host = torch.from_numpy(np.random.default_rng(1).uniform(-1.0, 1.0, N)).pin_memory()
+    out_host = torch.empty(N, dtype=torch.float64).pin_memory()
+    rd = torch.empty(N, dtype=torch.float64, device=dev)
+    od = torch.empty(N, dtype=torch.float64, device=dev)
+
+    def e2e_step():
+        rd.copy_(r_host, non_blocking=True)
+        V.apply_additive(ps, rd, od, scale=0.5, mode=L.VK_APPLY_XSET)
+        out_host.copy_(od, non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    te = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * J / (float(te.item()) * 1e-3)
+
+    # ---- MG-FGMRES(30) time-to-solution, fine grid b
+    solver = FgmresSolver(hier)
+    b = torch.from_numpy(mg_rhs(pack)).to(dev)
+    solver.solve(b)                           # warm-up (graph capture)
+    torch.cuda.synchronize()
+    tts = []
+    for _ in range(3):
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        xs, its, conv, hist = solver.solve(b)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        tts.append(s0.elapsed_time(s1))
+    ref_hist = None
+    hp = os.path.join(ROOT, "tests", "golden", f"{CONFIG}_history.json")
+    if os.path.exists(hp):
+        ref = json.load(open(hp))
+        ref_hist = np.asarray(ref["history"])
+    hist_rel = None
+    if ref_hist is not None:
+        m = min(len(hist), len(ref_hist))
+        hist_rel = float(np.max(np.abs(hist[:m] - ref_hist[:m]) / ref_hist[:m]))
+
+    # ---- fine-level SpMV / fused residual bandwidth
+    A = fine.A
+    y = torch.empty_like(r)
+    for _ in range(3):
+        L.call("vk_residual", A.handle, L.ptr(r), L.ptr(x), L.ptr(y), sp)
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q0.record(stream)
+    for _ in range(20):
+        L.call("vk_residual", A.handle, L.ptr(r), L.ptr(x), L.ptr(y), sp)
+    q1.record(stream)
+    torch.cuda.synchronize()
+    ms_res = q0.elapsed_time(q1) / 20
+    bytes_res = 12 * A.nnz + 4 * (N + 1) + 24 * N
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_kind = _peak_hbm()
+    achieved = bytes_solve / (ms_solve * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("patch_solve_kernel", {}).get("dram_bytes")
+        except Exception:
+            traffic = None
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu = cpu_sweep_sample(pack, steps=3, warmup=1)
+        cpu.pop("ms_per_step", None)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference-assembled operators (data/cfg2_pack.npz), seeded "
+                "uniform[-1,1] residual",
+        "config": {"workload": f"{CONFIG}: Taylor-Hood P2/P1, 256x256 right-triangle grid, "
+                               "finest level of the 5-level hierarchy; one additive Vanka "
+                               "sweep (damping 0.5) per step",
+                   "N": N, "patches": J, "sum_s": sum_s, "sum_s2": sum_s2,
+                   "l2": "inputs larger than L2 (8*sum s^2 = %.0f MB streamed per sweep)"
+                         % (8 * sum_s2 / 1e6),
+                   "parallelism": f"replicas x{world}"},
+        "roofline": {"bound": "hbm", "kernel": "patch_solve_kernel (K4a)",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes": bytes_solve, "ms": ms_solve},
+        "sweep": {"ms": ms_solve + ms_gather, "ms_solve": ms_solve, "ms_accumulate": ms_gather,
+                  "gbps": bytes_sweep / ((ms_solve + ms_gather) * 1e-3) / 1e9,
+                  "algorithmic_bytes": bytes_sweep},
+        "residual_spmv": {"ms": ms_res, "gbps": bytes_res / (ms_res * 1e-3) / 1e9,
+                          "nnz": int(A.nnz)},
+        "mg_fgmres": {"tts_ms_median": statistics.median(tts), "tts_ms": tts,
+                      "iterations": its, "converged": bool(conv),
+                      "reference_iterations": int(len(ref_hist) - 1) if ref_hist is not None else None,
+                      "history_max_rel_vs_reference": hist_rel, "setup_s": setup_s},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * N,
+                "d2h_bytes_per_step": 8 * N, "ms_per_step": ms_e2e},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

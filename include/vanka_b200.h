@@ -1,0 +1,169 @@
+/*
+ * vanka_b200.h — C ABI of the B200-native Vanka / multigrid hot path.
+ *
+ * Plain C types only (pointers, sizes, opaque handles, int status).  Every
+ * entry point names the reference interface it replaces (file:line under
+ * /root/reference/pkg/src/stokesmg/); see INTEGRATION.md for the ctypes
+ * binding the reference package would add.
+ *
+ * Conventions
+ *   - status: 0 ok; VK_ERR_* (< 0) argument / CUDA / allocation error, with a
+ *     message from vk_last_error(); factor reports per-patch singularity in
+ *     its status array and returns VK_SINGULAR (> 0).
+ *   - handles own their device memory; vectors are caller-owned DEVICE
+ *     pointers (fp64) unless the name says host.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *     all vector calls are asynchronous and stream-ordered, capturable in a
+ *     CUDA graph (no allocation, no host sync).
+ *   - array inputs to *_create / *_build may be host or device pointers
+ *     (copied with cudaMemcpyDefault).
+ */
+#ifndef VANKA_B200_H
+#define VANKA_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define VK_API __attribute__((visibility("default")))
+#else
+#define VK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VK_OK 0
+#define VK_SINGULAR 1
+#define VK_ERR_ARG (-1)
+#define VK_ERR_CUDA (-2)
+#define VK_ERR_ALLOC (-3)
+#define VK_ERR_UNSUPPORTED (-4)
+
+/* per-patch factor status (reference sparsela.py:76-83) */
+#define VK_PATCH_OK 0
+#define VK_PATCH_ZERO_ROW 1      /* "matrix has an all-zero row"            */
+#define VK_PATCH_SMALL_PIVOT 2   /* "pivot below 1e-12 of its row magnitude" */
+
+/* weighting (reference vanka.py:25) */
+#define VK_WEIGHT_INVMULT 0
+#define VK_WEIGHT_UNIT 1
+
+/* gather epilogues for vk_patches_apply (reference vanka.py:142-148 and the
+ * damped update of mg.py:268-271) */
+#define VK_APPLY_OUT 0           /* out  = sum_i R_i^T W_i A_i^-1 R_i r        */
+#define VK_APPLY_XSET 1          /* x    = scale * out        (x was zero)     */
+#define VK_APPLY_XADD 2          /* x    = x + scale * out                     */
+
+typedef struct vk_csr_s* vk_csr_t;
+typedef struct vk_patches_s* vk_patches_t;
+
+VK_API const char* vk_last_error(void);
+VK_API int vk_version(void);
+VK_API int vk_device_sync(void);
+
+/* ---------------- matrices: scipy.sparse.csr_matrix on the device ---------
+ * replaces the CSR the reference builds in assembly.py:288-332 / mg.py:159-167
+ * (consumed by sparsela.py:45-47, mg.py:41-45). */
+VK_API int vk_csr_create(const int32_t* indptr, const int32_t* indices, const double* data,
+                  int32_t nrows, int32_t ncols, int64_t nnz, vk_csr_t* out);
+/* transpose (masked.T for restriction, mg.py:44-45), deterministic order */
+VK_API int vk_csr_transpose(vk_csr_t a, vk_csr_t* out);
+VK_API int vk_csr_info(vk_csr_t a, int32_t* nrows, int32_t* ncols, int64_t* nnz);
+VK_API int vk_csr_destroy(vk_csr_t a);
+
+/* ---------------- SpMV (K5/K6) ---------------------------------------------
+ * y = alpha*A x + beta*y   : sparsela.spmv (sparsela.py:45-47), prolong
+ *                            (mg.py:41-42, with beta=1 for x + P e, mg.py:296)
+ * r = b - A x              : residual at mg.py:270, 294 */
+VK_API int vk_spmv(vk_csr_t a, const double* x, double* y, double alpha, double beta, void* stream);
+VK_API int vk_residual(vk_csr_t a, const double* b, const double* x, double* r, void* stream);
+
+/* ---------------- patches (K1-K4) ------------------------------------------
+ * vk_patches_build replaces vanka.build_patches_taylor_hood /
+ * build_patches_hdiv_extended / _finish (vanka.py:49-126).  Candidate patch
+ * p (in reference order: dim, entity index) owns the cells
+ * ent2cell[ent2cell_ptr[p] : ent2cell_ptr[p+1]] and the pressure DoFs
+ * pdofs[pdof_ptr[p] : pdof_ptr[p+1]] (already offset).  Velocity DoFs =
+ * sorted unique union of cell_dofs over those cells minus constrained
+ * (constrained[d] != 0).  Empty candidates are dropped (vanka.py:64-65). */
+VK_API int vk_patches_build(const int32_t* cell_dofs, int32_t ncells, int32_t nloc,
+                     const int32_t* ent2cell_ptr, const int32_t* ent2cell,
+                     int32_t ncand, const int32_t* pdof_ptr, const int32_t* pdofs,
+                     const uint8_t* constrained, int32_t ndof, int32_t weighting,
+                     vk_patches_t* out);
+/* patch set from explicit lists (reference Patch/PatchSet built by hand,
+ * vanka.py:28-46): offsets[npatch+1] (int64), indices[offsets[npatch]],
+ * num_velocity[npatch], weights[offsets[npatch]] (NULL = all ones);
+ * multiplicity is recomputed by counting. */
+VK_API int vk_patches_from_lists(const int64_t* offsets, const int32_t* indices,
+                          const int32_t* num_velocity, const double* weights,
+                          int32_t npatch, int32_t ndof, vk_patches_t* out);
+/* sizes: number of kept patches, total patch entries (sum s), max patch size */
+VK_API int vk_patches_info(vk_patches_t h, int32_t* npatch, int64_t* total, int32_t* smax);
+/* bit-exact export to HOST arrays (any may be NULL): offsets[npatch+1],
+ * indices[total], num_velocity[npatch], weights[total], multiplicity[ndof],
+ * cand_of_patch[npatch] (candidate index of each kept patch) */
+VK_API int vk_patches_export(vk_patches_t h, int64_t* offsets, int32_t* indices,
+                      int32_t* num_velocity, double* weights, double* multiplicity,
+                      int32_t* cand_of_patch);
+/* general dense extraction A[rows, cols] (sparsela.extract_submatrix,
+ * sparsela.py:50-60) into a DEVICE row-major nrows x ncols array; rows/cols
+ * are DEVICE int32 lists, sorted and duplicate-free (checked by the caller). */
+VK_API int vk_extract(vk_csr_t a, const int32_t* rows, int32_t nrows, const int32_t* cols,
+                      int32_t ncols, double* out_dev, void* stream);
+/* extract dense blocks A[idx, idx] (sparsela.extract_submatrix, sparsela.py:50-60)
+ * for patches first..first+count-1 into HOST row-major blocks concatenated in
+ * patch order (sum s^2 doubles). */
+VK_API int vk_patches_extract(vk_patches_t h, vk_csr_t a, int32_t first, int32_t count,
+                       double* blocks_host);
+/* extract + batched LU-with-partial-pivoting-equivalent Gauss-Jordan inverse
+ * with the reference row-scale guard (vanka.factor_patches, vanka.py:129-139;
+ * sparsela.lu_factor, sparsela.py:63-84).  status_host[npatch] (may be NULL)
+ * receives VK_PATCH_*; returns VK_SINGULAR if any patch is singular and
+ * first_bad (may be NULL) = its index. */
+VK_API int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_host, int32_t* first_bad);
+/* explicit patch inverses to HOST (row-major s x s per patch, concatenated) */
+VK_API int vk_patches_export_inverse(vk_patches_t h, int32_t first, int32_t count, double* inv_host);
+/* additive sweep (vanka.apply_additive, vanka.py:142-148, + mg.py:268-271):
+ * mode VK_APPLY_OUT: out = sum_i R_i^T W_i A_i^{-1} R_i r ; XSET/XADD: see above.
+ * Deterministic: contributions summed per DoF in patch order. */
+VK_API int vk_patches_apply(vk_patches_t h, const double* r, double* out, double scale,
+                     int32_t mode, void* stream);
+/* the two halves of vk_patches_apply, for per-kernel timing:
+ * solve: z = W A_i^{-1} R_i r into the handle's sum(s) buffer (K4a);
+ * accumulate: per-DoF patch-ordered sum of z + epilogue (K4b). */
+VK_API int vk_patches_solve(vk_patches_t h, const double* r, void* stream);
+VK_API int vk_patches_accumulate(vk_patches_t h, double* out, double scale, int32_t mode,
+                                 void* stream);
+VK_API int vk_patches_destroy(vk_patches_t h);
+
+/* ---------------- dense / vector helpers (FGMRES + V-cycle plumbing) -------
+ * sparsela.fgmres (sparsela.py:117-191), coarse_solve (mg.py:274-279),
+ * v_cycle bc copy (mg.py:298-300).  Device scalars are single doubles. */
+/* *out_dev = x . y  (deterministic two-level reduction, one launch) */
+VK_API int vk_dot(int64_t n, const double* x, const double* y, double* out_dev, void* stream);
+/* y = y - (*a_dev) * x */
+VK_API int vk_axpy_dev(int64_t n, const double* a_dev, const double* x, double* y, void* stream);
+/* y = y + a * x  (host scalar) */
+VK_API int vk_axpy(int64_t n, double a, const double* x, double* y, void* stream);
+/* y = x / (*d_dev) */
+VK_API int vk_div_dev(int64_t n, const double* x, const double* d_dev, double* y, void* stream);
+/* *out_dev = sqrt(x . x) */
+VK_API int vk_nrm2(int64_t n, const double* x, double* out_dev, void* stream);
+/* x = x - q (q . x) in place (NullspaceProjector, sparsela.py:113-114) */
+VK_API int vk_project(int64_t n, const double* q, double* x, double* scratch_dev, void* stream);
+/* dst[idx[k]] = src[idx[k]] */
+VK_API int vk_copy_index(int64_t m, const int32_t* idx, const double* src, double* dst, void* stream);
+/* y = M x for a dense row-major m x n matrix (coarse inverse apply) */
+VK_API int vk_gemv(int32_t m, int32_t n, const double* mat, const double* x, double* y, void* stream);
+/* x += sum_k coef_dev[k] * Z[k, :]  (Z row-major count x n): FGMRES update */
+VK_API int vk_combine(int64_t n, int32_t count, const double* z, const double* coef_dev,
+               double* x, void* stream);
+/* dense[rows x cols] (row-major, device) = CSR (coarse operator densify) */
+VK_API int vk_csr_to_dense(vk_csr_t a, double* dense, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VANKA_B200_H */

@@ -1,0 +1,22 @@
+"""B200-native (sm_100a) Vanka patch relaxation + multigrid hot path.
+
+Drop-in for the hot path of the reference package ``stokesmg``
+(arXiv 2409.14222 companion code): the names below mirror
+``stokesmg/__init__.py:29-35`` for ``sparsela``, ``vanka`` and ``mg``.  All
+numerics run in ``libvanka_b200.so`` (hand-written CUDA behind a C ABI,
+``include/vanka_b200.h``); importing works without a GPU, computing does not
+(no CPU fallback).
+"""
+
+from .pack import ProblemPack, read_pack
+from .sparsela import (DenseFactorization, DeviceCSR, KrylovReport, NullspaceProjector,
+                       SingularMatrixError, device_csr, estimate_lambda_max,
+                       extract_submatrix, fgmres, lu_factor, lu_solve, nullspace_projector,
+                       spmv, triple_product)
+from .vanka import (EntityRef, Patch, PatchSet, apply_additive, build_patches,
+                    build_patches_hdiv_extended, build_patches_taylor_hood, factor_patches)
+from .mg import (ChebyshevParams, FixedDamping, Level, MgHierarchy, TransferPair,
+                 chebyshev_iteration, chebyshev_relax, coarse_solve, hierarchy_from_pack,
+                 hierarchy_from_reference, make_preconditioner, pressure_kernel, v_cycle)
+
+__version__ = "0.1.0"

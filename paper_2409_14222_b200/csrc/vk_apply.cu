@@ -1,0 +1,159 @@
+// K4: the additive Vanka sweep (reference vanka.apply_additive,
+// vanka.py:142-148, with the damped update of mg.chebyshev_relax,
+// mg.py:268-271).
+//
+// Two stream-ordered kernels, no atomics, bit-reproducible:
+//   patch_solve_kernel — one warp per patch (persistent grid-stride over
+//     patches in build order so residual gathers stay local): gather
+//     r[idx] into a per-warp shared slice, stream the column-major explicit
+//     inverse with evict-first loads (the dominant 8*s^2 bytes), one row per
+//     lane (rows lane, lane+32, ...), then z = w (*) y  (fl(w*y), no FMA,
+//     exactly `p.weights * local`) into a sum(s)-long buffer.
+//   dof_gather_kernel — one thread per DoF sums its z entries in ascending
+//     patch order (the DoF->slot map), reproducing the reference's
+//     sequential `out[idx] += ...` order, and applies the epilogue
+//     out = acc | x = scale*acc | x = x + scale*acc.
+#include <algorithm>
+
+#include "vk_common.cuh"
+
+namespace {
+
+constexpr int kApplyWarps = 8;
+constexpr int kApplyMaxS = 192;
+
+template <int RPL>
+__device__ __forceinline__ void solve_one(int lane, int s, int64_t base, const double* __restrict__ A,
+                                          const double* __restrict__ w, const double* rsh,
+                                          double* __restrict__ z) {
+  double y[RPL];
+#pragma unroll
+  for (int q = 0; q < RPL; ++q) y[q] = 0.0;
+  constexpr int U = (RPL <= 2) ? 8 : 4;
+  int j = 0;
+  for (; j + U <= s; j += U) {
+    double a[U][RPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        const int i = lane + 32 * q;
+        a[u][q] = (i < s) ? __ldcs(A + (j + u) * s + i) : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double rj = rsh[j + u];
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) y[q] = fma(a[u][q], rj, y[q]);
+    }
+  }
+  for (; j < s; ++j) {
+    const double rj = rsh[j];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+      const int i = lane + 32 * q;
+      if (i < s) y[q] = fma(__ldcs(A + j * s + i), rj, y[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < RPL; ++q) {
+    const int i = lane + 32 * q;
+    if (i < s) z[base + i] = __dmul_rn(w[base + i], y[q]);
+  }
+}
+
+__global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_kernel(
+    int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
+    const double* __restrict__ w, const int64_t* __restrict__ opoff,
+    const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
+  __shared__ double rsh_all[kApplyWarps][kApplyMaxS];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  double* rsh = rsh_all[warp];
+  const int nwarps = gridDim.x * kApplyWarps;
+  for (int p = blockIdx.x * kApplyWarps + warp; p < npatch; p += nwarps) {
+    const int64_t base = off[p];
+    const int s = static_cast<int>(off[p + 1] - base);
+    for (int i = lane; i < s; i += 32) rsh[i] = __ldg(r + idx[base + i]);
+    __syncwarp();
+    const double* A = inv + opoff[p];
+    switch ((s + 31) >> 5) {
+      case 1: solve_one<1>(lane, s, base, A, w, rsh, z); break;
+      case 2: solve_one<2>(lane, s, base, A, w, rsh, z); break;
+      case 3: solve_one<3>(lane, s, base, A, w, rsh, z); break;
+      case 4: solve_one<4>(lane, s, base, A, w, rsh, z); break;
+      case 5: solve_one<5>(lane, s, base, A, w, rsh, z); break;
+      default: solve_one<6>(lane, s, base, A, w, rsh, z); break;
+    }
+    __syncwarp();
+  }
+}
+
+template <int MODE>
+__global__ void dof_gather_kernel(int ndof, const int* __restrict__ dptr, const int* __restrict__ dslot,
+                                  const double* __restrict__ z, double* __restrict__ out, double scale) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < ndof; d += gridDim.x * blockDim.x) {
+    const int k0 = dptr[d], k1 = dptr[d + 1];
+    double acc = 0.0;
+    for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, z[dslot[k]]);
+    if (MODE == VK_APPLY_OUT)
+      out[d] = acc;
+    else if (MODE == VK_APPLY_XSET)
+      out[d] = __dmul_rn(scale, acc);
+    else
+      out[d] = __dadd_rn(out[d], __dmul_rn(scale, acc));
+  }
+}
+
+}  // namespace
+
+static int check_apply(vk_patches_t h) {
+  VK_REQUIRE(h, "vk_patches_apply: null handle");
+  VK_REQUIRE(h->factored, "vk_patches_apply: patches are not factored");
+  VK_REQUIRE(h->smax <= kApplyMaxS, "vk_patches_apply: patch size %d > %d", h->smax, kApplyMaxS);
+  return VK_OK;
+}
+
+extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
+  if (int st = check_apply(h)) return st;
+  VK_REQUIRE(r, "vk_patches_solve: null residual");
+  if (h->npatch > 0) {
+    const int grid = std::min((h->npatch + kApplyWarps - 1) / kApplyWarps, 148 * 8);
+    patch_solve_kernel<<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(
+        h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf);
+  }
+  VK_CHECK_LAUNCH();
+  return VK_OK;
+}
+
+extern "C" int vk_patches_accumulate(vk_patches_t h, double* out, double scale, int32_t mode,
+                                     void* stream) {
+  if (int st = check_apply(h)) return st;
+  VK_REQUIRE(out, "vk_patches_accumulate: null output");
+  VK_REQUIRE(mode == VK_APPLY_OUT || mode == VK_APPLY_XSET || mode == VK_APPLY_XADD,
+             "vk_patches_apply: bad mode %d", mode);
+  cudaStream_t st = vk_stream(stream);
+  const int g2 = vk_grid(h->ndof, 256, 148 * 16);
+  if (h->ndof > 0) {
+    switch (mode) {
+      case VK_APPLY_OUT:
+        dof_gather_kernel<VK_APPLY_OUT><<<g2, 256, 0, st>>>(h->ndof, h->dptr, h->dslot, h->zbuf, out, scale);
+        break;
+      case VK_APPLY_XSET:
+        dof_gather_kernel<VK_APPLY_XSET><<<g2, 256, 0, st>>>(h->ndof, h->dptr, h->dslot, h->zbuf, out, scale);
+        break;
+      default:
+        dof_gather_kernel<VK_APPLY_XADD><<<g2, 256, 0, st>>>(h->ndof, h->dptr, h->dslot, h->zbuf, out, scale);
+        break;
+    }
+  }
+  VK_CHECK_LAUNCH();
+  return VK_OK;
+}
+
+extern "C" int vk_patches_apply(vk_patches_t h, const double* r, double* out, double scale,
+                                int32_t mode, void* stream) {
+  VK_REQUIRE(r && out, "vk_patches_apply: null argument");
+  if (int st = vk_patches_solve(h, r, stream)) return st;
+  return vk_patches_accumulate(h, out, scale, mode, stream);
+}

@@ -1,0 +1,404 @@
+// K2 + K3: patch submatrix extraction fused with a batched fp64 inverse.
+//
+// Reference: vanka.factor_patches (vanka.py:129-139) =
+//   extract_submatrix (sparsela.py:50-60)  -> dense A[idx, idx]
+//   lu_factor         (sparsela.py:63-84)  -> getrf + row-scale pivot guard
+// and the apply-time lu_solve (sparsela.py:87-90).
+//
+// One CTA per patch, block resident in shared memory (row-major, odd leading
+// dimension => conflict-free column access for 64-bit words):
+//   1. extraction: warp per block row, each lane binary-searches a CSR column
+//      of row idx[i] in the sorted patch index list; stored entries are copied
+//      verbatim (bit-exact), absent ones are +0.0.
+//   2. guard: row scale = max |A_ij| (all-zero row -> VK_PATCH_ZERO_ROW).
+//   3. in-place Gauss-Jordan with partial pivoting.  Pivot search breaks ties
+//      to the lowest row like LAPACK idamax; the pivot taken at step k is U_kk
+//      of the LU with partial pivoting, checked against 1e-12 * rowscale of
+//      its source row (VK_PATCH_SMALL_PIVOT) exactly like sparsela.py:79-83.
+//   4. the explicit inverse (same bytes as L\U, no triangular dependency at
+//      apply time) is written column-major with the column permutation undone.
+// Size classes: patches are bucketed by size so each launch sizes its
+// dynamic shared memory (and occupancy) to the bucket's largest block.
+#include <algorithm>
+#include <vector>
+
+#include "vk_common.cuh"
+
+namespace {
+
+constexpr int kMaxPatch = 164;  // s*(s|1)*8 + 20 s bytes <= 227 KB
+
+__host__ __device__ inline int lda_of(int s) { return s | 1; }
+
+inline size_t factor_smem_bytes(int s) {
+  return sizeof(double) * (size_t(s) * lda_of(s) + s) + sizeof(int) * 3 * size_t(s);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) factor_kernel(
+    const int* __restrict__ plist, int count, const int64_t* __restrict__ off,
+    const int* __restrict__ idx, const int* __restrict__ ptr, const int* __restrict__ col,
+    const double* __restrict__ val, const int64_t* __restrict__ opoff, double* __restrict__ inv,
+    int* __restrict__ status, double* __restrict__ blocks_out, const int64_t* __restrict__ blk_off,
+    int extract_only) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_piv;
+  __shared__ int s_status;
+  constexpr int NW = NT / 32;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  for (int b = blockIdx.x; b < count; b += gridDim.x) {
+    const int p = plist[b];
+    const int64_t base = off[p];
+    const int s = static_cast<int>(off[p + 1] - base);
+    const int ld = lda_of(s);
+    double* A = smem;
+    double* rs = A + size_t(s) * ld;
+    int* sidx = reinterpret_cast<int*>(rs + s);
+    int* perm = sidx + s;
+    int* iperm = perm + s;
+
+    for (int i = threadIdx.x; i < s; i += NT) {
+      sidx[i] = idx[base + i];
+      perm[i] = i;
+    }
+    for (int e = threadIdx.x; e < s * ld; e += NT) A[e] = 0.0;
+    if (threadIdx.x == 0) s_status = 0;
+    __syncthreads();
+
+    // 1. extraction (bit-exact copy of stored entries)
+    for (int i = warp; i < s; i += NW) {
+      const int row = sidx[i];
+      const int k0 = ptr[row], k1 = ptr[row + 1];
+      for (int k = k0 + lane; k < k1; k += 32) {
+        const int c = col[k];
+        int lo = 0, hi = s - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (sidx[mid] < c) lo = mid + 1; else hi = mid;
+        }
+        if (sidx[lo] == c) A[i * ld + lo] = val[k];
+      }
+    }
+    __syncthreads();
+    if (blocks_out) {
+      double* dst = blocks_out + blk_off[b];
+      for (int e = threadIdx.x; e < s * s; e += NT) dst[e] = A[(e / s) * ld + (e % s)];
+      if (extract_only) {
+        __syncthreads();
+        continue;
+      }
+    }
+
+    // 2. row scales and the all-zero-row guard (sparsela.py:76-78)
+    for (int i = warp; i < s; i += NW) {
+      double m = 0.0;
+      for (int j = lane; j < s; j += 32) m = fmax(m, fabs(A[i * ld + j]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) {
+        rs[i] = m;
+        if (m == 0.0) s_status = VK_PATCH_ZERO_ROW;
+      }
+    }
+    __syncthreads();
+    if (s_status != 0) {
+      if (threadIdx.x == 0) status[p] = s_status;
+      __syncthreads();
+      continue;
+    }
+
+    // 3. Gauss-Jordan with partial pivoting
+    for (int k = 0; k < s; ++k) {
+      if (warp == 0) {
+        double best = -1.0;
+        int bi = s;
+        for (int i = k + lane; i < s; i += 32) {
+          const double v = fabs(A[i * ld + k]);
+          if (v > best) {  // strict: first (lowest) row wins ties, like idamax
+            best = v;
+            bi = i;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+          }
+        }
+        if (lane == 0) {
+          s_piv = bi;
+          if (bi != k) {
+            const int t = perm[k];
+            perm[k] = perm[bi];
+            perm[bi] = t;
+          }
+        }
+      }
+      __syncthreads();
+      const int pr = s_piv;
+      if (pr != k) {
+        for (int j = threadIdx.x; j < s; j += NT) {
+          const double t = A[k * ld + j];
+          A[k * ld + j] = A[pr * ld + j];
+          A[pr * ld + j] = t;
+        }
+      }
+      __syncthreads();
+      const double piv = A[k * ld + k];
+      if (!(fabs(piv) >= 1e-12 * rs[perm[k]])) {  // also catches NaN
+        if (threadIdx.x == 0) s_status = VK_PATCH_SMALL_PIVOT;
+        break;  // block-uniform: every thread sees the same piv
+      }
+      const double rinv = 1.0 / piv;
+      __syncthreads();  // everyone has read piv before row k changes
+      for (int j = threadIdx.x; j < s; j += NT)
+        A[k * ld + j] = (j == k) ? rinv : A[k * ld + j] * rinv;
+      __syncthreads();
+      for (int i = warp; i < s; i += NW) {
+        if (i == k) continue;
+        const double f = A[i * ld + k];
+        __syncwarp();
+        for (int j = lane; j < s; j += 32) {
+          if (j == k)
+            A[i * ld + k] = -f * rinv;
+          else
+            A[i * ld + j] = fma(-f, A[k * ld + j], A[i * ld + j]);
+        }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (s_status != 0) {
+      if (threadIdx.x == 0) status[p] = s_status;
+      __syncthreads();
+      continue;
+    }
+    // 4. inverse of A = X P (X = inverse of the row-permuted block):
+    //    Ainv[i][j] = X[i][iperm[j]], written column-major.
+    for (int q = threadIdx.x; q < s; q += NT) iperm[perm[q]] = q;
+    __syncthreads();
+    double* dst = inv + opoff[p];
+    for (int e = threadIdx.x; e < s * s; e += NT) {
+      const int j = e / s, i = e - j * s;
+      dst[e] = A[i * ld + iperm[j]];
+    }
+    if (threadIdx.x == 0) status[p] = VK_PATCH_OK;
+    __syncthreads();
+  }
+}
+
+// generic A[rows, cols]: warp per output row, binary search of each stored
+// column in the sorted `cols` list; stored values copied verbatim.
+__global__ void extract_kernel(const int* __restrict__ ptr, const int* __restrict__ col,
+                               const double* __restrict__ val, const int* __restrict__ rows, int nr,
+                               const int* __restrict__ cols, int nc, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nr; i += nw) {
+    double* o = out + int64_t(i) * nc;
+    for (int j = lane; j < nc; j += 32) o[j] = 0.0;
+    __syncwarp();
+    const int r = rows[i];
+    for (int k = ptr[r] + lane; k < ptr[r + 1]; k += 32) {
+      const int c = col[k];
+      int lo = 0, hi = nc - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cols[mid] < c) lo = mid + 1; else hi = mid;
+      }
+      if (cols[lo] == c) o[lo] = val[k];
+    }
+    __syncwarp();
+  }
+}
+
+struct Bucket {
+  int smax;
+  std::vector<int> ids;
+};
+
+std::vector<Bucket> make_buckets(const std::vector<int64_t>& off, int first, int count) {
+  static const int edges[] = {16, 32, 48, 64, 80, 96, 112, 128, 144, kMaxPatch};
+  std::vector<Bucket> b(sizeof(edges) / sizeof(int));
+  for (size_t i = 0; i < b.size(); ++i) b[i].smax = edges[i];
+  for (int p = first; p < first + count; ++p) {
+    const int s = static_cast<int>(off[p + 1] - off[p]);
+    for (auto& bk : b)
+      if (s <= bk.smax) {
+        bk.ids.push_back(p);
+        break;
+      }
+  }
+  return b;
+}
+
+int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int* d_status,
+                  double* blocks, const std::vector<int64_t>* blk_off_host, int extract_only,
+                  cudaStream_t st) {
+  if (bk.ids.empty()) return VK_OK;
+  int* d_ids = nullptr;
+  int64_t* d_boff = nullptr;
+  VK_CHECK_CUDA(cudaMalloc(&d_ids, sizeof(int) * bk.ids.size()));
+  VK_CHECK_CUDA(cudaMemcpy(d_ids, bk.ids.data(), sizeof(int) * bk.ids.size(), cudaMemcpyHostToDevice));
+  if (blk_off_host) {
+    VK_CHECK_CUDA(cudaMalloc(&d_boff, sizeof(int64_t) * blk_off_host->size()));
+    VK_CHECK_CUDA(cudaMemcpy(d_boff, blk_off_host->data(), sizeof(int64_t) * blk_off_host->size(),
+                             cudaMemcpyHostToDevice));
+  }
+  const size_t smem = factor_smem_bytes(bk.smax);
+  const int count = static_cast<int>(bk.ids.size());
+  if (bk.smax <= 32) {
+    VK_CHECK_CUDA(cudaFuncSetAttribute(factor_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(smem)));
+    factor_kernel<128><<<std::min(count, 148 * 32), 128, smem, st>>>(
+        d_ids, count, h->off, h->idx, a->indptr, a->indices, a->data, h->opoff, h->inv, d_status,
+        blocks, d_boff, extract_only);
+  } else {
+    VK_CHECK_CUDA(cudaFuncSetAttribute(factor_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(smem)));
+    factor_kernel<256><<<std::min(count, 148 * 16), 256, smem, st>>>(
+        d_ids, count, h->off, h->idx, a->indptr, a->indices, a->data, h->opoff, h->inv, d_status,
+        blocks, d_boff, extract_only);
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(d_ids);
+  cudaFree(d_boff);
+  if (e != cudaSuccess) {
+    vk::set_error("factor_kernel: %s", cudaGetErrorString(e));
+    return VK_ERR_CUDA;
+  }
+  return VK_OK;
+}
+
+}  // namespace
+
+extern "C" int vk_extract(vk_csr_t a, const int32_t* rows, int32_t nrows, const int32_t* cols,
+                          int32_t ncols, double* out_dev, void* stream) {
+  VK_REQUIRE(a && rows && cols && out_dev && nrows > 0 && ncols > 0, "vk_extract: bad argument");
+  const int grid = std::min((nrows + 7) / 8, 148 * 8);
+  extract_kernel<<<grid, 256, 0, vk_stream(stream)>>>(a->indptr, a->indices, a->data, rows, nrows, cols,
+                                                      ncols, out_dev);
+  VK_CHECK_LAUNCH();
+  return VK_OK;
+}
+
+extern "C" int vk_patches_extract(vk_patches_t h, vk_csr_t a, int32_t first, int32_t count,
+                                  double* blocks_host) {
+  VK_REQUIRE(h && a && blocks_host, "vk_patches_extract: null argument");
+  VK_REQUIRE(first >= 0 && count >= 0 && first + count <= h->npatch, "vk_patches_extract: range");
+  VK_REQUIRE(a->nrows == h->ndof && a->ncols == h->ndof, "vk_patches_extract: matrix is %dx%d, patches need %d",
+             a->nrows, a->ncols, h->ndof);
+  if (count == 0) return VK_OK;
+  VK_REQUIRE(h->smax <= kMaxPatch, "patch size %d exceeds %d", h->smax, kMaxPatch);
+  auto buckets = make_buckets(h->h_off, first, count);
+  // block offsets in patch order
+  std::vector<int64_t> rel(count + 1, 0);
+  for (int q = 0; q < count; ++q) {
+    const int64_t s = h->h_off[first + q + 1] - h->h_off[first + q];
+    rel[q + 1] = rel[q] + s * s;
+  }
+  double* d_blocks = nullptr;
+  int* d_status = nullptr;
+  VK_CHECK_CUDA(cudaMalloc(&d_blocks, sizeof(double) * std::max<int64_t>(rel[count], 1)));
+  VK_CHECK_CUDA(cudaMalloc(&d_status, sizeof(int) * h->npatch));
+  int st = VK_OK;
+  for (auto& bk : buckets) {
+    std::vector<int64_t> boff(bk.ids.size());
+    for (size_t q = 0; q < bk.ids.size(); ++q) boff[q] = rel[bk.ids[q] - first];
+    st = launch_bucket(bk, h, a, d_status, d_blocks, &boff, 1, 0);
+    if (st) break;
+  }
+  if (!st) {
+    cudaError_t e = cudaMemcpy(blocks_host, d_blocks, sizeof(double) * rel[count], cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      vk::set_error("vk_patches_extract: %s", cudaGetErrorString(e));
+      st = VK_ERR_CUDA;
+    }
+  }
+  cudaFree(d_blocks);
+  cudaFree(d_status);
+  return st;
+}
+
+extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_host, int32_t* first_bad) {
+  VK_REQUIRE(h && a, "vk_patches_factor: null argument");
+  VK_REQUIRE(a->nrows == h->ndof && a->ncols == h->ndof,
+             "vk_patches_factor: matrix is %dx%d, patches need %d", a->nrows, a->ncols, h->ndof);
+  if (h->smax > kMaxPatch) {
+    vk::set_error("vk_patches_factor: patch size %d exceeds the shared-memory limit %d", h->smax,
+                  kMaxPatch);
+    return VK_ERR_UNSUPPORTED;
+  }
+  // operator storage: s^2 rounded to even (16-byte aligned per patch)
+  std::vector<int64_t> oo(h->npatch + 1, 0);
+  for (int p = 0; p < h->npatch; ++p) {
+    const int64_t s = h->h_off[p + 1] - h->h_off[p];
+    oo[p + 1] = oo[p] + ((s * s + 1) & ~int64_t(1));
+  }
+  if (!h->opoff) VK_CHECK_CUDA(cudaMalloc(&h->opoff, sizeof(int64_t) * (h->npatch + 1)));
+  VK_CHECK_CUDA(cudaMemcpy(h->opoff, oo.data(), sizeof(int64_t) * (h->npatch + 1), cudaMemcpyHostToDevice));
+  if (h->inv && h->inv_total != oo[h->npatch]) {
+    cudaFree(h->inv);
+    h->inv = nullptr;
+  }
+  if (!h->inv) {
+    VK_CHECK_CUDA(cudaMalloc(&h->inv, sizeof(double) * std::max<int64_t>(oo[h->npatch], 2)));
+    h->inv_total = oo[h->npatch];
+  }
+  int* d_status = nullptr;
+  VK_CHECK_CUDA(cudaMalloc(&d_status, sizeof(int) * std::max(h->npatch, 1)));
+  VK_CHECK_CUDA(cudaMemset(d_status, 0, sizeof(int) * std::max(h->npatch, 1)));
+  auto buckets = make_buckets(h->h_off, 0, h->npatch);
+  int st = VK_OK;
+  for (auto& bk : buckets) {
+    st = launch_bucket(bk, h, a, d_status, nullptr, nullptr, 0, 0);
+    if (st) break;
+  }
+  std::vector<int32_t> hs(h->npatch);
+  if (!st && h->npatch) {
+    cudaError_t e = cudaMemcpy(hs.data(), d_status, sizeof(int) * h->npatch, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      vk::set_error("vk_patches_factor: %s", cudaGetErrorString(e));
+      st = VK_ERR_CUDA;
+    }
+  }
+  cudaFree(d_status);
+  if (st) return st;
+  if (status_host) std::copy(hs.begin(), hs.end(), status_host);
+  int bad = -1;
+  for (int p = 0; p < h->npatch; ++p)
+    if (hs[p] != VK_PATCH_OK) {
+      bad = p;
+      break;
+    }
+  if (first_bad) *first_bad = bad;
+  h->factored = (bad < 0);
+  if (bad >= 0) {
+    vk::set_error("singular patch block at patch %d (status %d)", bad, hs[bad]);
+    return VK_SINGULAR;
+  }
+  return VK_OK;
+}
+
+extern "C" int vk_patches_export_inverse(vk_patches_t h, int32_t first, int32_t count, double* inv_host) {
+  VK_REQUIRE(h && inv_host, "vk_patches_export_inverse: null argument");
+  VK_REQUIRE(h->factored, "vk_patches_export_inverse: patches not factored");
+  VK_REQUIRE(first >= 0 && count >= 0 && first + count <= h->npatch, "vk_patches_export_inverse: range");
+  std::vector<int64_t> oo(h->npatch + 1);
+  VK_CHECK_CUDA(cudaMemcpy(oo.data(), h->opoff, sizeof(int64_t) * (h->npatch + 1), cudaMemcpyDeviceToHost));
+  int64_t w = 0;
+  for (int p = first; p < first + count; ++p) {
+    const int64_t s = h->h_off[p + 1] - h->h_off[p];
+    std::vector<double> cm(s * s);
+    if (s) VK_CHECK_CUDA(cudaMemcpy(cm.data(), h->inv + oo[p], sizeof(double) * s * s, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < s; ++i)
+      for (int64_t j = 0; j < s; ++j) inv_host[w + i * s + j] = cm[j * s + i];
+    w += s * s;
+  }
+  return VK_OK;
+}
