@@ -22,68 +22,114 @@ namespace {
 constexpr int kApplyWarps = 8;
 constexpr int kApplyMaxS = 192;
 
-template <int RPL>
-__device__ __forceinline__ void solve_one(int lane, int s, int64_t base, const double* __restrict__ A,
-                                          const double* __restrict__ w, const double* rsh,
-                                          double* __restrict__ z) {
-  double y[RPL];
-#pragma unroll
-  for (int q = 0; q < RPL; ++q) y[q] = 0.0;
-  constexpr int U = (RPL <= 2) ? 8 : 4;
-  int j = 0;
-  for (; j + U <= s; j += U) {
-    double a[U][RPL];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) {
-        const int i = lane + 32 * q;
-        a[u][q] = (i < s) ? __ldcs(A + (j + u) * s + i) : 0.0;
-      }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const double rj = rsh[j + u];
-#pragma unroll
-      for (int q = 0; q < RPL; ++q) y[q] = fma(a[u][q], rj, y[q]);
-    }
-  }
-  for (; j < s; ++j) {
-    const double rj = rsh[j];
-#pragma unroll
-    for (int q = 0; q < RPL; ++q) {
-      const int i = lane + 32 * q;
-      if (i < s) y[q] = fma(__ldcs(A + j * s + i), rj, y[q]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < RPL; ++q) {
-    const int i = lane + 32 * q;
-    if (i < s) z[base + i] = __dmul_rn(w[base + i], y[q]);
-  }
-}
-
+// Rows-per-lane R = ceil(smax / 32) is a template parameter; every patch of
+// the launch uses R row slots per lane (predicated by i < s).
+//
+// The per-patch prologue (offsets -> index list -> residual gather) is a
+// chain of dependent loads; it is software-pipelined three patches deep so
+// each stage has a whole patch's operator stream to land: at the top of
+// patch p the warp stores r_p (gathered during patch p-1) to shared memory,
+// issues the residual gathers of p+1 (indices loaded during p-1), the index
+// loads of p+2 (offsets loaded during p-1) and the offset loads of p+3, and
+// only then streams patch p's operator.
+template <int R>
 __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_kernel(
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
-  __shared__ double rsh_all[kApplyWarps][kApplyMaxS];
+  constexpr int U = (R == 1) ? 8 : (R == 2 ? 4 : 2);
+  __shared__ double rsh_all[kApplyWarps][32 * R];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   double* rsh = rsh_all[warp];
-  const int nwarps = gridDim.x * kApplyWarps;
-  for (int p = blockIdx.x * kApplyWarps + warp; p < npatch; p += nwarps) {
-    const int64_t base = off[p];
-    const int s = static_cast<int>(off[p + 1] - base);
-    for (int i = lane; i < s; i += 32) rsh[i] = __ldg(r + idx[base + i]);
+  const int nw = gridDim.x * kApplyWarps;
+  const int p0 = blockIdx.x * kApplyWarps + warp;
+
+  // pipeline registers: stage A (r values), B (indices), C (offsets)
+  int64_t baseA = 0, opA = 0, baseB = 0, opB = 0, baseC = 0, opC = 0;
+  int sA = 0, sB = 0, sC = 0;
+  double rA[R];
+  int iB[R];
+  auto load_meta = [&](int p, int64_t& base, int& sz, int64_t& op) {
+    if (p < npatch) {
+      base = off[p];
+      sz = static_cast<int>(off[p + 1] - base);
+      op = opoff[p];
+    } else {
+      base = 0;
+      sz = 0;
+      op = 0;
+    }
+  };
+  // fill: A = p0, B = p0 + nw, C = p0 + 2 nw
+  load_meta(p0, baseA, sA, opA);
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int i = lane + 32 * q;
+    rA[q] = (i < sA) ? __ldg(r + idx[baseA + i]) : 0.0;
+  }
+  load_meta(p0 + nw, baseB, sB, opB);
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int i = lane + 32 * q;
+    iB[q] = (i < sB) ? idx[baseB + i] : 0;
+  }
+  load_meta(p0 + 2 * nw, baseC, sC, opC);
+
+  for (int p = p0; p < npatch; p += nw) {
+    const int64_t base = baseA, ob = opA;
+    const int s = sA;
+#pragma unroll
+    for (int q = 0; q < R; ++q) rsh[lane + 32 * q] = rA[q];
+    // advance the pipeline (loads land while patch p streams)
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = lane + 32 * q;
+      rA[q] = (i < sB) ? __ldg(r + iB[q]) : 0.0;
+    }
+    baseA = baseB; opA = opB; sA = sB;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = lane + 32 * q;
+      iB[q] = (i < sC) ? idx[baseC + i] : 0;
+    }
+    baseB = baseC; opB = opC; sB = sC;
+    load_meta(p + 3 * nw, baseC, sC, opC);
     __syncwarp();
-    const double* A = inv + opoff[p];
-    switch ((s + 31) >> 5) {
-      case 1: solve_one<1>(lane, s, base, A, w, rsh, z); break;
-      case 2: solve_one<2>(lane, s, base, A, w, rsh, z); break;
-      case 3: solve_one<3>(lane, s, base, A, w, rsh, z); break;
-      case 4: solve_one<4>(lane, s, base, A, w, rsh, z); break;
-      case 5: solve_one<5>(lane, s, base, A, w, rsh, z); break;
-      default: solve_one<6>(lane, s, base, A, w, rsh, z); break;
+
+    const double* A = inv + ob;
+    double y[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) y[q] = 0.0;
+    int j = 0;
+    for (; j + U <= s; j += U) {
+      double a[U][R];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = lane + 32 * q;
+          a[u][q] = (i < s) ? __ldcs(A + (j + u) * s + i) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double rj = rsh[j + u];
+#pragma unroll
+        for (int q = 0; q < R; ++q) y[q] = fma(a[u][q], rj, y[q]);
+      }
+    }
+    for (; j < s; ++j) {
+      const double rj = rsh[j];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = lane + 32 * q;
+        if (i < s) y[q] = fma(__ldcs(A + j * s + i), rj, y[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = lane + 32 * q;
+      if (i < s) z[base + i] = __dmul_rn(w[base + i], y[q]);
     }
     __syncwarp();
   }
@@ -119,8 +165,19 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
   VK_REQUIRE(r, "vk_patches_solve: null residual");
   if (h->npatch > 0) {
     const int grid = std::min((h->npatch + kApplyWarps - 1) / kApplyWarps, 148 * 8);
-    patch_solve_kernel<<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(
-        h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf);
+    const int rpl = (h->smax + 31) / 32;
+#define VK_SOLVE(RV)                                                                      \
+  patch_solve_kernel<RV><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(               \
+      h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf)
+    switch (rpl) {
+      case 1: VK_SOLVE(1); break;
+      case 2: VK_SOLVE(2); break;
+      case 3: VK_SOLVE(3); break;
+      case 4: VK_SOLVE(4); break;
+      case 5: VK_SOLVE(5); break;
+      default: VK_SOLVE(6); break;
+    }
+#undef VK_SOLVE
   }
   VK_CHECK_LAUNCH();
   return VK_OK;

@@ -1,17 +1,21 @@
 // K5/K6: CSR matrices on the device, SpMV / fused residual / transfers.
 //
 // Replaces scipy csr_matvec at reference sparsela.py:45-47 (spmv),
-// mg.py:41-45 (TransferPair.prolong / restrict, restrict via an explicit
+// mg.py:41-45 (TransferPair.prolong / restrict — restrict through an explicit
 // transposed CSR), mg.py:270, 294 (residual b - A x).
 //
-// HBM-bound (0.17 flop/B): a sub-warp of VPR lanes owns a row; each lane
-// streams UNROLL (col, val) pairs per batch with evict-first loads so the
-// L2-resident x / b vectors (<= 5.4 MB) are not displaced by the matrix
-// stream; sub-warp shuffle reduction.
+// CSR-stream kernel (HBM-bound, 0.17 flop/B): the rows are cut on the host
+// into blocks of <= 2048 nonzeros / 512 rows.  A 256-thread CTA owns one
+// block: every thread issues 8 independent coalesced (col, val) loads plus
+// the 8 x-gathers (x is L2-resident), and stores the products in shared
+// memory; then each row is summed sequentially, left to right, without FMA
+// contraction: y_i = ((0 + a_i0 x_0) + a_i1 x_1) + ...  — the exact
+// operation order of scipy's csr_matvec (and, through the ascending-source
+// transpose, of csc_matvec for masked.T), so SpMV / residual / transfers are
+// bit-identical to the reference.
 #include <algorithm>
 #include <cstdarg>
 #include <cstring>
-#include <mutex>
 #include <numeric>
 #include <string>
 
@@ -39,60 +43,77 @@ extern "C" int vk_device_sync(void) {
 
 namespace {
 
-__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
-__device__ __forceinline__ int ld_stream(const int* p) { return __ldcs(p); }
+using vk::kStreamNnz;
+using vk::kStreamRows;
+using vk::kStreamThreads;
+using vk::kStreamU;
 
-// mode 0: y = alpha*Ax + beta*y   (beta == 0: y not read)
-// mode 1: y = b - A x
-template <int VPR, int UNROLL, int MODE>
-__global__ void __launch_bounds__(256) spmv_kernel(int nrows, const int* __restrict__ ptr,
-                                                   const int* __restrict__ col,
-                                                   const double* __restrict__ val,
-                                                   const double* __restrict__ x,
-                                                   double* __restrict__ y, double alpha,
-                                                   double beta, const double* __restrict__ b) {
-  const int lane = threadIdx.x & (VPR - 1);
-  constexpr int ROWS_PER_WARP = 32 / VPR;
-  const int warps_per_block = blockDim.x >> 5;
-  const int warp = threadIdx.x >> 5;
-  const int sub = (threadIdx.x & 31) / VPR;
-  const int64_t step = int64_t(gridDim.x) * warps_per_block * ROWS_PER_WARP;
-  // warp-uniform trip count so every lane reaches the shuffles
-  for (int64_t base = (int64_t(blockIdx.x) * warps_per_block + warp) * ROWS_PER_WARP; base < nrows;
-       base += step) {
-    const int row = static_cast<int>(base) + sub;
-    const bool active = row < nrows;
-    const int start = active ? __ldg(ptr + row) : 0;
-    const int end = active ? __ldg(ptr + row + 1) : 0;
-    double sum = 0.0;
-    for (int k0 = start + lane; k0 < end; k0 += VPR * UNROLL) {
-      int c[UNROLL];
-      double v[UNROLL];
+// MODE 0: y = alpha*Ax + beta*y (beta == 0: y not read);  MODE 1: y = b - A x
+template <int MODE>
+__global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
+    const int* __restrict__ rowblk, const int* __restrict__ ptr, const int* __restrict__ col,
+    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+    double alpha, double beta, const double* __restrict__ b) {
+  __shared__ double prod[kStreamNnz];
+  __shared__ int sptr[kStreamRows + 1];
+  __shared__ double carry;
+  const int t = threadIdx.x;
+  const int r0 = rowblk[blockIdx.x], r1 = rowblk[blockIdx.x + 1];
+  const int nr = r1 - r0;
+  for (int i = t; i <= nr; i += kStreamThreads) sptr[i] = ptr[r0 + i];
+  __syncthreads();
+  const int k0 = sptr[0], k1 = sptr[nr];
+  const bool single = (nr == 1);
+  if (t == 0) carry = 0.0;
+  for (int kc = k0; kc < k1 || (kc == k0 && k0 == k1); kc += kStreamNnz) {
+    const int kend = min(k1, kc + kStreamNnz);
+    int c[kStreamU];
+    double v[kStreamU];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        const int k = k0 + u * VPR;
-        if (k < end) {
-          c[u] = ld_stream(col + k);
-          v[u] = ld_stream(val + k);
-        } else {
-          c[u] = -1;
-          v[u] = 0.0;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < UNROLL; ++u)
-        if (c[u] >= 0) sum = fma(v[u], __ldg(x + c[u]), sum);
+    for (int u = 0; u < kStreamU; ++u) {
+      const int k = kc + t + u * kStreamThreads;
+      c[u] = (k < kend) ? __ldcs(col + k) : 0;
+      v[u] = (k < kend) ? __ldcs(val + k) : 0.0;
     }
 #pragma unroll
-    for (int off = VPR / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off, VPR);
-    if (lane == 0 && active) {
-      if (MODE == 1) {
-        y[row] = __dsub_rn(b[row], sum);
-      } else {
-        double out = (alpha == 1.0) ? sum : __dmul_rn(alpha, sum);
-        if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[row] : __dmul_rn(beta, y[row]), out);
-        y[row] = out;
+    for (int u = 0; u < kStreamU; ++u) {
+      const int k = kc + t + u * kStreamThreads;
+      if (k < kend) prod[k - kc] = __dmul_rn(v[u], __ldg(x + c[u]));
+    }
+    __syncthreads();
+    if (single) {
+      // a row longer than one chunk: thread 0 carries the sequential sum
+      if (t == 0) {
+        double s = carry;
+        for (int k = kc; k < kend; ++k) s = __dadd_rn(s, prod[k - kc]);
+        carry = s;
       }
+    } else {
+      for (int i = t; i < nr; i += kStreamThreads) {
+        const int a = sptr[i] - kc, e = sptr[i + 1] - kc;
+        double s = 0.0;
+        for (int k = a; k < e; ++k) s = __dadd_rn(s, prod[k]);
+        const int row = r0 + i;
+        if (MODE == 1) {
+          y[row] = __dsub_rn(b[row], s);
+        } else {
+          double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
+          if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[row] : __dmul_rn(beta, y[row]), out);
+          y[row] = out;
+        }
+      }
+    }
+    __syncthreads();
+    if (k0 == k1) break;
+  }
+  if (single && t == 0) {
+    const double s = carry;
+    if (MODE == 1) {
+      y[r0] = __dsub_rn(b[r0], s);
+    } else {
+      double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
+      if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[r0] : __dmul_rn(beta, y[r0]), out);
+      y[r0] = out;
     }
   }
 }
@@ -100,33 +121,9 @@ __global__ void __launch_bounds__(256) spmv_kernel(int nrows, const int* __restr
 template <int MODE>
 cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alpha, double beta,
                         const double* b, cudaStream_t st) {
-  const int block = 256;
-  // lanes per row from the mean row length (P2 ~26, P4/Q3/BDM3 ~60-70,
-  // transfers 2-39)
-  const double m = a.mean_row;
-  int vpr = m > 48 ? 32 : (m > 20 ? 16 : (m > 10 ? 8 : 4));
-  const int64_t groups = a.nrows;
-  const int per_block = block / vpr;
-  int grid = static_cast<int>(std::min<int64_t>((groups + per_block - 1) / per_block, 148 * 64));
-  if (grid < 1) grid = 1;
-  switch (vpr) {
-    case 32:
-      spmv_kernel<32, 2, MODE><<<grid, block, 0, st>>>(a.nrows, a.indptr, a.indices, a.data, x, y,
-                                                       alpha, beta, b);
-      break;
-    case 16:
-      spmv_kernel<16, 2, MODE><<<grid, block, 0, st>>>(a.nrows, a.indptr, a.indices, a.data, x, y,
-                                                       alpha, beta, b);
-      break;
-    case 8:
-      spmv_kernel<8, 2, MODE><<<grid, block, 0, st>>>(a.nrows, a.indptr, a.indices, a.data, x, y,
-                                                      alpha, beta, b);
-      break;
-    default:
-      spmv_kernel<4, 2, MODE><<<grid, block, 0, st>>>(a.nrows, a.indptr, a.indices, a.data, x, y,
-                                                      alpha, beta, b);
-      break;
-  }
+  if (a.nblocks == 0) return cudaSuccess;
+  csr_stream_kernel<MODE><<<a.nblocks, kStreamThreads, 0, st>>>(a.rowblk, a.indptr, a.indices,
+                                                               a.data, x, y, alpha, beta, b);
   return cudaGetLastError();
 }
 
@@ -142,21 +139,54 @@ __global__ void csr_to_dense_kernel(int nrows, int ncols, const int* __restrict_
   }
 }
 
+// greedy row blocks: <= kStreamNnz nonzeros and <= kStreamRows rows; a row
+// longer than kStreamNnz gets a block of its own
+std::vector<int32_t> make_row_blocks(const std::vector<int32_t>& p) {
+  const int32_t n = static_cast<int32_t>(p.size()) - 1;
+  std::vector<int32_t> rb;
+  rb.push_back(0);
+  int32_t r = 0;
+  while (r < n) {
+    int32_t start = r;
+    int64_t nnz = 0;
+    while (r < n && r - start < kStreamRows) {
+      const int64_t len = p[r + 1] - p[r];
+      if (r > start && nnz + len > kStreamNnz) break;
+      nnz += len;
+      ++r;
+      if (nnz > kStreamNnz) break;  // single long row
+    }
+    rb.push_back(r);
+  }
+  return rb;
+}
+
 }  // namespace
 
 extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, const double* data,
                              int32_t nrows, int32_t ncols, int64_t nnz, vk_csr_t* out) {
   VK_REQUIRE(out != nullptr && nrows >= 0 && ncols >= 0 && nnz >= 0, "vk_csr_create: bad args");
   VK_REQUIRE(nnz < (int64_t(1) << 31), "vk_csr_create: nnz exceeds int32 indexing");
+  std::vector<int32_t> hp(nrows + 1);
+  cudaError_t e = cudaMemcpy(hp.data(), indptr, sizeof(int32_t) * (nrows + 1), cudaMemcpyDefault);
+  if (e != cudaSuccess) {
+    vk::set_error("vk_csr_create: %s", cudaGetErrorString(e));
+    return VK_ERR_CUDA;
+  }
+  VK_REQUIRE(hp[0] == 0 && hp[nrows] == nnz, "vk_csr_create: indptr does not match nnz");
+  auto rb = make_row_blocks(hp);
   auto* a = new vk_csr_s();
   a->nrows = nrows;
   a->ncols = ncols;
   a->nnz = nnz;
-  cudaError_t e = cudaMalloc(&a->indptr, sizeof(int32_t) * (nrows + 1));
+  a->nblocks = static_cast<int32_t>(rb.size()) - 1;
+  e = cudaMalloc(&a->indptr, sizeof(int32_t) * (nrows + 1));
   if (e == cudaSuccess) e = cudaMalloc(&a->indices, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
   if (e == cudaSuccess) e = cudaMalloc(&a->data, sizeof(double) * std::max<int64_t>(nnz, 1));
+  if (e == cudaSuccess) e = cudaMalloc(&a->rowblk, sizeof(int32_t) * rb.size());
   if (e == cudaSuccess)
-    e = cudaMemcpy(a->indptr, indptr, sizeof(int32_t) * (nrows + 1), cudaMemcpyDefault);
+    e = cudaMemcpy(a->indptr, hp.data(), sizeof(int32_t) * (nrows + 1), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(a->rowblk, rb.data(), sizeof(int32_t) * rb.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && nnz)
     e = cudaMemcpy(a->indices, indices, sizeof(int32_t) * nnz, cudaMemcpyDefault);
   if (e == cudaSuccess && nnz) e = cudaMemcpy(a->data, data, sizeof(double) * nnz, cudaMemcpyDefault);
@@ -165,12 +195,10 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
     cudaFree(a->indptr);
     cudaFree(a->indices);
     cudaFree(a->data);
+    cudaFree(a->rowblk);
     delete a;
     return VK_ERR_CUDA;
   }
-  // row statistics for the launch heuristic
-  std::vector<int32_t> hp(nrows + 1);
-  cudaMemcpy(hp.data(), a->indptr, sizeof(int32_t) * (nrows + 1), cudaMemcpyDeviceToHost);
   int32_t mx = 0;
   for (int32_t i = 0; i < nrows; ++i) mx = std::max(mx, hp[i + 1] - hp[i]);
   a->max_row = mx;
@@ -181,9 +209,9 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
 
 extern "C" int vk_csr_transpose(vk_csr_t a, vk_csr_t* out) {
   VK_REQUIRE(a && out, "vk_csr_transpose: null handle");
-  // Deterministic counting transpose (entries of each output row in
-  // ascending source-row order, i.e. the summation order of scipy's
-  // csc_matvec on masked.T).  Setup-only; done on the host.
+  // Deterministic counting transpose: the entries of each output row come in
+  // ascending source-row order, i.e. the accumulation order of scipy's
+  // csc_matvec on masked.T (mg.py:44-45).  Setup-only; done on the host.
   const int64_t nnz = a->nnz;
   std::vector<int32_t> p(a->nrows + 1), c(nnz);
   std::vector<double> v(nnz);
@@ -219,6 +247,7 @@ extern "C" int vk_csr_destroy(vk_csr_t a) {
   cudaFree(a->indptr);
   cudaFree(a->indices);
   cudaFree(a->data);
+  cudaFree(a->rowblk);
   delete a;
   return VK_OK;
 }

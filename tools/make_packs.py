@@ -54,6 +54,23 @@ CASES = {
     "s_bdm3": ("bdm", 3, 4, 1),
     "s_rt2": ("rt", 2, 4, 1),
     "s_thquad2": ("th-quad", 2, 3, 2),
+    # tiny single-level cases mirroring the reference's own unit tests
+    # (tests/test_vanka.py:23-124)
+    "t_thtri2_5": ("th-tri", 2, 5, None),
+    "t_thtri4_5": ("th-tri", 4, 5, None),
+    "t_thquad3_5": ("th-quad", 3, 5, None),
+    "t_bdm1_5": ("bdm", 1, 5, None),
+    "t_rt1_5": ("rt", 1, 5, None),
+    "t_thtri3_3": ("th-tri", 3, 3, None),
+    "t_thquad2_3": ("th-quad", 2, 3, None),
+    "t_bdm2_3": ("bdm", 2, 3, None),
+    "t_rt1_3": ("rt", 1, 3, None),
+    "t_thtri2_3": ("th-tri", 2, 3, None),
+    "t_thquad3_2": ("th-quad", 3, 2, None),
+    "t_bdm1_3": ("bdm", 1, 3, None),
+    "t_thquad2_2": ("th-quad", 2, 2, None),
+    "t_thtri2_2": ("th-tri", 2, 2, None),
+    "t_bdm1_2": ("bdm", 1, 2, None),
 }
 FULL = ("cfg2", "cfg3", "cfg4", "cfg5")
 
