@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_kernel(
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
-  constexpr int U = (R == 1) ? 8 : (R == 2 ? 4 : 2);
+  constexpr int U = (R <= 2) ? 8 : (R <= 4 ? 4 : 2);
   __shared__ double rsh_all[kApplyWarps][32 * R];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -101,29 +101,22 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_kernel(
     double y[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) y[q] = 0.0;
-    int j = 0;
-    for (; j + U <= s; j += U) {
+    // column groups of U, the last one predicated (no scalar tail): every
+    // group keeps U*R independent loads in flight per lane
+    for (int j = 0; j < s; j += U) {
       double a[U][R];
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int q = 0; q < R; ++q) {
           const int i = lane + 32 * q;
-          a[u][q] = (i < s) ? __ldcs(A + (j + u) * s + i) : 0.0;
+          a[u][q] = (i < s && j + u < s) ? __ldcs(A + (j + u) * s + i) : 0.0;
         }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const double rj = rsh[j + u];
+        const double rj = (j + u < s) ? rsh[j + u] : 0.0;
 #pragma unroll
         for (int q = 0; q < R; ++q) y[q] = fma(a[u][q], rj, y[q]);
-      }
-    }
-    for (; j < s; ++j) {
-      const double rj = rsh[j];
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int i = lane + 32 * q;
-        if (i < s) y[q] = fma(__ldcs(A + j * s + i), rj, y[q]);
       }
     }
 #pragma unroll
