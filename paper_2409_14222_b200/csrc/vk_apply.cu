@@ -146,6 +146,95 @@ __global__ void dof_gather_kernel(int ndof, const int* __restrict__ dptr, const 
 
 }  // namespace
 
+namespace {
+
+// Variant for large / mixed patch sizes: one warp per row-chunk task
+// (patch p, rows 32c .. 32c+31).  Every warp keeps one row per lane (low
+// register count => high occupancy) and U independent column loads in
+// flight; the task's residual gather (all s entries) goes through the same
+// three-deep prologue pipeline as the per-patch kernel.
+template <int RMAX, int U>
+__global__ void __launch_bounds__(kApplyWarps * 32) patch_task_kernel(
+    int ntask, const int2* __restrict__ tasks, const int64_t* __restrict__ off,
+    const int* __restrict__ idx, const double* __restrict__ w, const int64_t* __restrict__ opoff,
+    const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
+  __shared__ double rsh_all[kApplyWarps][32 * RMAX];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  double* rsh = rsh_all[warp];
+  const int nw = gridDim.x * kApplyWarps;
+  const int t0 = blockIdx.x * kApplyWarps + warp;
+
+  int64_t baseA = 0, opA = 0, baseB = 0, opB = 0, baseC = 0, opC = 0;
+  int sA = 0, sB = 0, sC = 0, cA = 0, cB = 0, cC = 0;
+  double rA[RMAX];
+  int iB[RMAX];
+  auto load_meta = [&](int t, int64_t& base, int& sz, int64_t& op, int& ch) {
+    if (t < ntask) {
+      const int2 tk = tasks[t];
+      base = off[tk.x];
+      sz = static_cast<int>(off[tk.x + 1] - base);
+      op = opoff[tk.x];
+      ch = tk.y;
+    } else {
+      base = 0;
+      sz = 0;
+      op = 0;
+      ch = 0;
+    }
+  };
+  load_meta(t0, baseA, sA, opA, cA);
+#pragma unroll
+  for (int q = 0; q < RMAX; ++q) {
+    const int i = lane + 32 * q;
+    rA[q] = (i < sA) ? __ldg(r + idx[baseA + i]) : 0.0;
+  }
+  load_meta(t0 + nw, baseB, sB, opB, cB);
+#pragma unroll
+  for (int q = 0; q < RMAX; ++q) {
+    const int i = lane + 32 * q;
+    iB[q] = (i < sB) ? idx[baseB + i] : 0;
+  }
+  load_meta(t0 + 2 * nw, baseC, sC, opC, cC);
+
+  for (int t = t0; t < ntask; t += nw) {
+    const int64_t base = baseA, ob = opA;
+    const int s = sA, chunk = cA;
+#pragma unroll
+    for (int q = 0; q < RMAX; ++q) rsh[lane + 32 * q] = rA[q];
+#pragma unroll
+    for (int q = 0; q < RMAX; ++q) {
+      const int i = lane + 32 * q;
+      rA[q] = (i < sB) ? __ldg(r + iB[q]) : 0.0;
+    }
+    baseA = baseB; opA = opB; sA = sB; cA = cB;
+#pragma unroll
+    for (int q = 0; q < RMAX; ++q) {
+      const int i = lane + 32 * q;
+      iB[q] = (i < sC) ? idx[baseC + i] : 0;
+    }
+    baseB = baseC; opB = opC; sB = sC; cB = cC;
+    load_meta(t + 3 * nw, baseC, sC, opC, cC);
+    __syncwarp();
+
+    const int row = 32 * chunk + lane;
+    const bool live = row < s;
+    const double* A = inv + ob + row;
+    double y = 0.0;
+    for (int j = 0; j < s; j += U) {
+      double a[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) a[u] = (live && j + u < s) ? __ldcs(A + (j + u) * s) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) y = fma(a[u], (j + u < s) ? rsh[j + u] : 0.0, y);
+    }
+    if (live) z[base + row] = __dmul_rn(w[base + row], y);
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
 static int check_apply(vk_patches_t h) {
   VK_REQUIRE(h, "vk_patches_apply: null handle");
   VK_REQUIRE(h->factored, "vk_patches_apply: patches are not factored");
@@ -153,12 +242,33 @@ static int check_apply(vk_patches_t h) {
   return VK_OK;
 }
 
+extern "C" int vk_patches_set_variant(vk_patches_t h, int32_t variant) {
+  VK_REQUIRE(h, "vk_patches_set_variant: null handle");
+  VK_REQUIRE(variant >= -1 && variant <= 1, "vk_patches_set_variant: bad variant %d", variant);
+  h->solve_variant = variant < 0 ? (h->smax > 64 ? 1 : 0) : variant;
+  return VK_OK;
+}
+
 extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
   if (int st = check_apply(h)) return st;
   VK_REQUIRE(r, "vk_patches_solve: null residual");
-  if (h->npatch > 0) {
+  const int rpl = (h->smax + 31) / 32;
+  if (h->npatch > 0 && h->solve_variant == 1 && h->ntask > 0) {
+    const int grid = std::min((h->ntask + kApplyWarps - 1) / kApplyWarps, 148 * 8);
+#define VK_TASK(RV)                                                                         \
+  patch_task_kernel<RV, 8><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(               \
+      h->ntask, h->tasks, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf)
+    switch (rpl) {
+      case 1: VK_TASK(1); break;
+      case 2: VK_TASK(2); break;
+      case 3: VK_TASK(3); break;
+      case 4: VK_TASK(4); break;
+      case 5: VK_TASK(5); break;
+      default: VK_TASK(6); break;
+    }
+#undef VK_TASK
+  } else if (h->npatch > 0) {
     const int grid = std::min((h->npatch + kApplyWarps - 1) / kApplyWarps, 148 * 8);
-    const int rpl = (h->smax + 31) / 32;
 #define VK_SOLVE(RV)                                                                      \
   patch_solve_kernel<RV><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(               \
       h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf)
