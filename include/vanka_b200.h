@@ -136,9 +136,6 @@ VK_API int vk_patches_apply(vk_patches_t h, const double* r, double* out, double
 VK_API int vk_patches_solve(vk_patches_t h, const double* r, void* stream);
 VK_API int vk_patches_accumulate(vk_patches_t h, double* out, double scale, int32_t mode,
                                  void* stream);
-/* apply kernel variant: 0 = warp per patch, 1 = warp per 32-row chunk,
- * -1 = heuristic (default after factor: 1 iff max patch size > 64) */
-VK_API int vk_patches_set_variant(vk_patches_t h, int32_t variant);
 VK_API int vk_patches_destroy(vk_patches_t h);
 
 /* ---------------- dense / vector helpers (FGMRES + V-cycle plumbing) -------

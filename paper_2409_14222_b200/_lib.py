@@ -49,7 +49,6 @@ SIGNATURES = {
     "vk_patches_apply": (C.c_int, [_p, _p, _p, _f64, _i32, _p]),
     "vk_patches_solve": (C.c_int, [_p, _p, _p]),
     "vk_patches_accumulate": (C.c_int, [_p, _p, _f64, _i32, _p]),
-    "vk_patches_set_variant": (C.c_int, [_p, _i32]),
     "vk_patches_destroy": (C.c_int, [_p]),
     "vk_dot": (C.c_int, [_i64, _p, _p, _p, _p]),
     "vk_axpy_dev": (C.c_int, [_i64, _p, _p, _p, _p]),

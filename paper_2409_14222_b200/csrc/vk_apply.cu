@@ -4,11 +4,10 @@
 //
 // Two stream-ordered kernels, no atomics, bit-reproducible:
 //   patch_solve_kernel — one warp per patch (persistent grid-stride over
-//     patches in build order so residual gathers stay local): gather
-//     r[idx] into a per-warp shared slice, stream the column-major explicit
-//     inverse with evict-first loads (the dominant 8*s^2 bytes), one row per
-//     lane (rows lane, lane+32, ...), then z = w (*) y  (fl(w*y), no FMA,
-//     exactly `p.weights * local`) into a sum(s)-long buffer.
+//     patches in build order so residual gathers stay local): stream the
+//     column-major explicit inverse with evict-first loads (the dominant
+//     8*s^2 bytes), rows lane, lane+32, ... per lane, then z = w (*) y
+//     (fl(w*y), exactly `p.weights * local`) into a sum(s)-long buffer.
 //   dof_gather_kernel — one thread per DoF sums its z entries in ascending
 //     patch order (the DoF->slot map), reproducing the reference's
 //     sequential `out[idx] += ...` order, and applies the epilogue
@@ -22,8 +21,42 @@ namespace {
 constexpr int kApplyWarps = 8;
 constexpr int kApplyMaxS = 192;
 
-// Rows-per-lane R = ceil(smax / 32) is a template parameter; every patch of
-// the launch uses R row slots per lane (predicated by i < s).
+// y = A_p^{-1} r_p for rows lane + 32 q (q < R), column groups of U with the
+// last group predicated (no scalar tail): U*R independent loads per lane.
+template <int R, int U>
+__device__ __forceinline__ void stream_patch(int lane, int s, int64_t base,
+                                             const double* __restrict__ A,
+                                             const double* __restrict__ w, const double* rsh,
+                                             double* __restrict__ z) {
+  double y[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) y[q] = 0.0;
+  for (int j = 0; j < s; j += U) {
+    double a[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = lane + 32 * q;
+        a[u][q] = (i < s && j + u < s) ? __ldcs(A + (j + u) * s + i) : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double rj = (j + u < s) ? rsh[j + u] : 0.0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) y[q] = fma(a[u][q], rj, y[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int i = lane + 32 * q;
+    if (i < s) z[base + i] = __dmul_rn(w[base + i], y[q]);
+  }
+}
+
+// RMAX = ceil(smax / 32) sizes the prologue registers; each patch streams
+// with its own R = ceil(s / 32) (warp-uniform switch), so mixed-size sets
+// (P4: 31/52/123, Q3: 33/57/99) do not pay for the largest class.
 //
 // The per-patch prologue (offsets -> index list -> residual gather) is a
 // chain of dependent loads; it is software-pipelined three patches deep so
@@ -32,13 +65,12 @@ constexpr int kApplyMaxS = 192;
 // issues the residual gathers of p+1 (indices loaded during p-1), the index
 // loads of p+2 (offsets loaded during p-1) and the offset loads of p+3, and
 // only then streams patch p's operator.
-template <int R>
+template <int RMAX>
 __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_kernel(
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
-  constexpr int U = (R <= 2) ? 8 : (R <= 4 ? 4 : 2);
-  __shared__ double rsh_all[kApplyWarps][32 * R];
+  __shared__ double rsh_all[kApplyWarps][32 * RMAX];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   double* rsh = rsh_all[warp];
@@ -48,8 +80,8 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_kernel(
   // pipeline registers: stage A (r values), B (indices), C (offsets)
   int64_t baseA = 0, opA = 0, baseB = 0, opB = 0, baseC = 0, opC = 0;
   int sA = 0, sB = 0, sC = 0;
-  double rA[R];
-  int iB[R];
+  double rA[RMAX];
+  int iB[RMAX];
   auto load_meta = [&](int p, int64_t& base, int& sz, int64_t& op) {
     if (p < npatch) {
       base = off[p];
@@ -61,16 +93,15 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_kernel(
       op = 0;
     }
   };
-  // fill: A = p0, B = p0 + nw, C = p0 + 2 nw
   load_meta(p0, baseA, sA, opA);
 #pragma unroll
-  for (int q = 0; q < R; ++q) {
+  for (int q = 0; q < RMAX; ++q) {
     const int i = lane + 32 * q;
     rA[q] = (i < sA) ? __ldg(r + idx[baseA + i]) : 0.0;
   }
   load_meta(p0 + nw, baseB, sB, opB);
 #pragma unroll
-  for (int q = 0; q < R; ++q) {
+  for (int q = 0; q < RMAX; ++q) {
     const int i = lane + 32 * q;
     iB[q] = (i < sB) ? idx[baseB + i] : 0;
   }
@@ -80,16 +111,16 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_kernel(
     const int64_t base = baseA, ob = opA;
     const int s = sA;
 #pragma unroll
-    for (int q = 0; q < R; ++q) rsh[lane + 32 * q] = rA[q];
+    for (int q = 0; q < RMAX; ++q) rsh[lane + 32 * q] = rA[q];
     // advance the pipeline (loads land while patch p streams)
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
+    for (int q = 0; q < RMAX; ++q) {
       const int i = lane + 32 * q;
       rA[q] = (i < sB) ? __ldg(r + iB[q]) : 0.0;
     }
     baseA = baseB; opA = opB; sA = sB;
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
+    for (int q = 0; q < RMAX; ++q) {
       const int i = lane + 32 * q;
       iB[q] = (i < sC) ? idx[baseC + i] : 0;
     }
@@ -98,31 +129,19 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_kernel(
     __syncwarp();
 
     const double* A = inv + ob;
-    double y[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) y[q] = 0.0;
-    // column groups of U, the last one predicated (no scalar tail): every
-    // group keeps U*R independent loads in flight per lane
-    for (int j = 0; j < s; j += U) {
-      double a[U][R];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const int i = lane + 32 * q;
-          a[u][q] = (i < s && j + u < s) ? __ldcs(A + (j + u) * s + i) : 0.0;
-        }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const double rj = (j + u < s) ? rsh[j + u] : 0.0;
-#pragma unroll
-        for (int q = 0; q < R; ++q) y[q] = fma(a[u][q], rj, y[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int i = lane + 32 * q;
-      if (i < s) z[base + i] = __dmul_rn(w[base + i], y[q]);
+    const int rp = (s + 31) >> 5;
+    if (RMAX <= 1 || rp <= 1) {
+      stream_patch<1, 16>(lane, s, base, A, w, rsh, z);
+    } else if (RMAX <= 2 || rp == 2) {
+      stream_patch<2, 8>(lane, s, base, A, w, rsh, z);
+    } else if (RMAX <= 3 || rp == 3) {
+      stream_patch<3, 4>(lane, s, base, A, w, rsh, z);
+    } else if (RMAX <= 4 || rp == 4) {
+      stream_patch<4, 4>(lane, s, base, A, w, rsh, z);
+    } else if (RMAX <= 5 || rp == 5) {
+      stream_patch<5, 2>(lane, s, base, A, w, rsh, z);
+    } else {
+      stream_patch<6, 2>(lane, s, base, A, w, rsh, z);
     }
     __syncwarp();
   }
@@ -146,95 +165,6 @@ __global__ void dof_gather_kernel(int ndof, const int* __restrict__ dptr, const 
 
 }  // namespace
 
-namespace {
-
-// Variant for large / mixed patch sizes: one warp per row-chunk task
-// (patch p, rows 32c .. 32c+31).  Every warp keeps one row per lane (low
-// register count => high occupancy) and U independent column loads in
-// flight; the task's residual gather (all s entries) goes through the same
-// three-deep prologue pipeline as the per-patch kernel.
-template <int RMAX, int U>
-__global__ void __launch_bounds__(kApplyWarps * 32) patch_task_kernel(
-    int ntask, const int2* __restrict__ tasks, const int64_t* __restrict__ off,
-    const int* __restrict__ idx, const double* __restrict__ w, const int64_t* __restrict__ opoff,
-    const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
-  __shared__ double rsh_all[kApplyWarps][32 * RMAX];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  double* rsh = rsh_all[warp];
-  const int nw = gridDim.x * kApplyWarps;
-  const int t0 = blockIdx.x * kApplyWarps + warp;
-
-  int64_t baseA = 0, opA = 0, baseB = 0, opB = 0, baseC = 0, opC = 0;
-  int sA = 0, sB = 0, sC = 0, cA = 0, cB = 0, cC = 0;
-  double rA[RMAX];
-  int iB[RMAX];
-  auto load_meta = [&](int t, int64_t& base, int& sz, int64_t& op, int& ch) {
-    if (t < ntask) {
-      const int2 tk = tasks[t];
-      base = off[tk.x];
-      sz = static_cast<int>(off[tk.x + 1] - base);
-      op = opoff[tk.x];
-      ch = tk.y;
-    } else {
-      base = 0;
-      sz = 0;
-      op = 0;
-      ch = 0;
-    }
-  };
-  load_meta(t0, baseA, sA, opA, cA);
-#pragma unroll
-  for (int q = 0; q < RMAX; ++q) {
-    const int i = lane + 32 * q;
-    rA[q] = (i < sA) ? __ldg(r + idx[baseA + i]) : 0.0;
-  }
-  load_meta(t0 + nw, baseB, sB, opB, cB);
-#pragma unroll
-  for (int q = 0; q < RMAX; ++q) {
-    const int i = lane + 32 * q;
-    iB[q] = (i < sB) ? idx[baseB + i] : 0;
-  }
-  load_meta(t0 + 2 * nw, baseC, sC, opC, cC);
-
-  for (int t = t0; t < ntask; t += nw) {
-    const int64_t base = baseA, ob = opA;
-    const int s = sA, chunk = cA;
-#pragma unroll
-    for (int q = 0; q < RMAX; ++q) rsh[lane + 32 * q] = rA[q];
-#pragma unroll
-    for (int q = 0; q < RMAX; ++q) {
-      const int i = lane + 32 * q;
-      rA[q] = (i < sB) ? __ldg(r + iB[q]) : 0.0;
-    }
-    baseA = baseB; opA = opB; sA = sB; cA = cB;
-#pragma unroll
-    for (int q = 0; q < RMAX; ++q) {
-      const int i = lane + 32 * q;
-      iB[q] = (i < sC) ? idx[baseC + i] : 0;
-    }
-    baseB = baseC; opB = opC; sB = sC; cB = cC;
-    load_meta(t + 3 * nw, baseC, sC, opC, cC);
-    __syncwarp();
-
-    const int row = 32 * chunk + lane;
-    const bool live = row < s;
-    const double* A = inv + ob + row;
-    double y = 0.0;
-    for (int j = 0; j < s; j += U) {
-      double a[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) a[u] = (live && j + u < s) ? __ldcs(A + (j + u) * s) : 0.0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) y = fma(a[u], (j + u < s) ? rsh[j + u] : 0.0, y);
-    }
-    if (live) z[base + row] = __dmul_rn(w[base + row], y);
-    __syncwarp();
-  }
-}
-
-}  // namespace
-
 static int check_apply(vk_patches_t h) {
   VK_REQUIRE(h, "vk_patches_apply: null handle");
   VK_REQUIRE(h->factored, "vk_patches_apply: patches are not factored");
@@ -242,33 +172,12 @@ static int check_apply(vk_patches_t h) {
   return VK_OK;
 }
 
-extern "C" int vk_patches_set_variant(vk_patches_t h, int32_t variant) {
-  VK_REQUIRE(h, "vk_patches_set_variant: null handle");
-  VK_REQUIRE(variant >= -1 && variant <= 1, "vk_patches_set_variant: bad variant %d", variant);
-  h->solve_variant = variant < 0 ? (h->smax > 64 ? 1 : 0) : variant;
-  return VK_OK;
-}
-
 extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
   if (int st = check_apply(h)) return st;
   VK_REQUIRE(r, "vk_patches_solve: null residual");
-  const int rpl = (h->smax + 31) / 32;
-  if (h->npatch > 0 && h->solve_variant == 1 && h->ntask > 0) {
-    const int grid = std::min((h->ntask + kApplyWarps - 1) / kApplyWarps, 148 * 8);
-#define VK_TASK(RV)                                                                         \
-  patch_task_kernel<RV, 8><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(               \
-      h->ntask, h->tasks, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf)
-    switch (rpl) {
-      case 1: VK_TASK(1); break;
-      case 2: VK_TASK(2); break;
-      case 3: VK_TASK(3); break;
-      case 4: VK_TASK(4); break;
-      case 5: VK_TASK(5); break;
-      default: VK_TASK(6); break;
-    }
-#undef VK_TASK
-  } else if (h->npatch > 0) {
+  if (h->npatch > 0) {
     const int grid = std::min((h->npatch + kApplyWarps - 1) / kApplyWarps, 148 * 8);
+    const int rpl = (h->smax + 31) / 32;
 #define VK_SOLVE(RV)                                                                      \
   patch_solve_kernel<RV><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(               \
       h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf)

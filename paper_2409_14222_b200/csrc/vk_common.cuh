@@ -51,9 +51,6 @@ struct Patches {
   int32_t* dptr = nullptr;      // [ndof+1] DoF -> slot map offsets
   int32_t* dslot = nullptr;     // [total] slots (flat patch entry ids), patch order
   double* zbuf = nullptr;       // [total] weighted local corrections
-  int32_t ntask = 0;            // row-chunk tasks (patch, 32-row chunk)
-  int2* tasks = nullptr;
-  int32_t solve_variant = 0;    // 0: warp per patch, 1: warp per row-chunk task
   bool factored = false;
   // host copies of the schedule (sizes) for bucketing
   std::vector<int64_t> h_off;

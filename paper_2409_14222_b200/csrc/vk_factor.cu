@@ -378,20 +378,6 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
     }
   if (first_bad) *first_bad = bad;
   h->factored = (bad < 0);
-  // row-chunk task list for the large/mixed-size apply variant
-  std::vector<int2> tk;
-  for (int p = 0; p < h->npatch; ++p) {
-    const int s = static_cast<int>(h->h_off[p + 1] - h->h_off[p]);
-    for (int c = 0; 32 * c < s; ++c) tk.push_back(make_int2(p, c));
-  }
-  cudaFree(h->tasks);
-  h->tasks = nullptr;
-  h->ntask = static_cast<int32_t>(tk.size());
-  if (!tk.empty()) {
-    VK_CHECK_CUDA(cudaMalloc(&h->tasks, sizeof(int2) * tk.size()));
-    VK_CHECK_CUDA(cudaMemcpy(h->tasks, tk.data(), sizeof(int2) * tk.size(), cudaMemcpyHostToDevice));
-  }
-  h->solve_variant = (h->smax > 64) ? 1 : 0;
   if (bad >= 0) {
     vk::set_error("singular patch block at patch %d (status %d)", bad, hs[bad]);
     return VK_SINGULAR;

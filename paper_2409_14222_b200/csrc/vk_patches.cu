@@ -231,7 +231,6 @@ void vk_patches_free(vk_patches_s* h) {
   cudaFree(h->dptr);
   cudaFree(h->dslot);
   cudaFree(h->zbuf);
-  cudaFree(h->tasks);
   delete h;
 }
 

@@ -72,11 +72,6 @@ def main():
         x = torch.zeros_like(r)
         y = torch.zeros_like(r)
         h = ps.handle
-        variants = {}
-        for v in (0, 1):
-            L.call("vk_patches_set_variant", h, v)
-            variants[v] = timed(lambda: L.call("vk_patches_solve", h, L.ptr(r), sp_), args.reps, st)
-        L.call("vk_patches_set_variant", h, -1)
         t_solve = timed(lambda: L.call("vk_patches_solve", h, L.ptr(r), sp_), args.reps, st)
         t_acc = timed(lambda: L.call("vk_patches_accumulate", h, L.ptr(x), 0.5, L.VK_APPLY_XADD, sp_),
                       args.reps, st)
@@ -85,9 +80,7 @@ def main():
         rec = {"N": N, "J": J, "nnz": int(A.nnz), "sum_s": s1, "sum_s2": s2, "smax": int(sz.max()),
                "build_s": t_build, "factor_s": t_factor,
                "factor_gflops_lu_equiv": (2.0 / 3.0) * s3 / t_factor / 1e9,
-               "solve_ms": t_solve, "solve_ms_patch_variant": variants[0],
-               "solve_ms_task_variant": variants[1],
-               "accumulate_ms": t_acc, "residual_ms": t_res}
+               "solve_ms": t_solve, "accumulate_ms": t_acc, "residual_ms": t_res}
         b_solve = 8 * s2 + 20 * s1 + 8 * N
         b_sweep = 8 * s2 + 12 * s1 + 16 * N
         b_res = 12 * A.nnz + 4 * (N + 1) + 24 * N
