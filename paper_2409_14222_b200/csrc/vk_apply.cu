@@ -65,7 +65,9 @@ __device__ __forceinline__ void stream_patch(int lane, int s, int64_t base,
 // issues the residual gathers of p+1 (indices loaded during p-1), the index
 // loads of p+2 (offsets loaded during p-1) and the offset loads of p+3, and
 // only then streams patch p's operator.
-template <int RMAX>
+__host__ __device__ constexpr int unroll_of(int r) { return r <= 2 ? 8 : (r <= 4 ? 4 : 2); }
+
+template <int RMAX, bool DISPATCH>
 __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_kernel(
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
@@ -129,19 +131,23 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_kernel(
     __syncwarp();
 
     const double* A = inv + ob;
-    const int rp = (s + 31) >> 5;
-    if (RMAX <= 1 || rp <= 1) {
-      stream_patch<1, 16>(lane, s, base, A, w, rsh, z);
-    } else if (RMAX <= 2 || rp == 2) {
-      stream_patch<2, 8>(lane, s, base, A, w, rsh, z);
-    } else if (RMAX <= 3 || rp == 3) {
-      stream_patch<3, 4>(lane, s, base, A, w, rsh, z);
-    } else if (RMAX <= 4 || rp == 4) {
-      stream_patch<4, 4>(lane, s, base, A, w, rsh, z);
-    } else if (RMAX <= 5 || rp == 5) {
-      stream_patch<5, 2>(lane, s, base, A, w, rsh, z);
+    if (!DISPATCH) {
+      stream_patch<RMAX, unroll_of(RMAX)>(lane, s, base, A, w, rsh, z);
     } else {
-      stream_patch<6, 2>(lane, s, base, A, w, rsh, z);
+      const int rp = (s + 31) >> 5;
+      if (RMAX <= 1 || rp <= 1) {
+        stream_patch<1, unroll_of(1)>(lane, s, base, A, w, rsh, z);
+      } else if (RMAX <= 2 || rp == 2) {
+        stream_patch<2, unroll_of(2)>(lane, s, base, A, w, rsh, z);
+      } else if (RMAX <= 3 || rp == 3) {
+        stream_patch<3, unroll_of(3)>(lane, s, base, A, w, rsh, z);
+      } else if (RMAX <= 4 || rp == 4) {
+        stream_patch<4, unroll_of(4)>(lane, s, base, A, w, rsh, z);
+      } else if (RMAX <= 5 || rp == 5) {
+        stream_patch<5, unroll_of(5)>(lane, s, base, A, w, rsh, z);
+      } else {
+        stream_patch<6, unroll_of(6)>(lane, s, base, A, w, rsh, z);
+      }
     }
     __syncwarp();
   }
@@ -178,9 +184,13 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
   if (h->npatch > 0) {
     const int grid = std::min((h->npatch + kApplyWarps - 1) / kApplyWarps, 148 * 8);
     const int rpl = (h->smax + 31) / 32;
-#define VK_SOLVE(RV)                                                                      \
-  patch_solve_kernel<RV><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(               \
-      h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf)
+#define VK_SOLVE(RV)                                                                        \
+  if (h->mixed_sizes)                                                                       \
+    patch_solve_kernel<RV, true><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(         \
+        h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf);                     \
+  else                                                                                      \
+    patch_solve_kernel<RV, false><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(        \
+        h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf)
     switch (rpl) {
       case 1: VK_SOLVE(1); break;
       case 2: VK_SOLVE(2); break;

@@ -51,6 +51,7 @@ struct Patches {
   int32_t* dptr = nullptr;      // [ndof+1] DoF -> slot map offsets
   int32_t* dslot = nullptr;     // [total] slots (flat patch entry ids), patch order
   double* zbuf = nullptr;       // [total] weighted local corrections
+  bool mixed_sizes = false;     // >25% of patches need fewer row slots than the largest
   bool factored = false;
   // host copies of the schedule (sizes) for bucketing
   std::vector<int64_t> h_off;

@@ -378,6 +378,15 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
     }
   if (first_bad) *first_bad = bad;
   h->factored = (bad < 0);
+  // apply schedule: per-patch row-slot dispatch pays off for mixed size
+  // classes (P4: 31/52/123, Q3: 33/57/99), not for uniform ones (P2, BDM3)
+  {
+    const int rmax = (h->smax + 31) / 32;
+    int64_t small = 0;
+    for (int p = 0; p < h->npatch; ++p)
+      if ((h->h_off[p + 1] - h->h_off[p] + 31) / 32 < rmax) ++small;
+    h->mixed_sizes = (4 * small > h->npatch);
+  }
   if (bad >= 0) {
     vk::set_error("singular patch block at patch %d (status %d)", bad, hs[bad]);
     return VK_SINGULAR;
