@@ -24,6 +24,14 @@ struct Csr {
   // CSR-stream schedule: row blocks of <= kStreamNnz nonzeros / kStreamRows rows
   int32_t nblocks = 0;
   int32_t* rowblk = nullptr;   // [nblocks+1]
+  // block-local column compression: per row block the sorted unique columns
+  // (ucol[ucolptr[b] .. ucolptr[b+1])) and a 16-bit local index per nonzero
+  int32_t* ucolptr = nullptr;  // [nblocks+1]
+  int32_t* ucol = nullptr;     // [sum of unique columns]
+  uint16_t* lidx = nullptr;    // [nnz] (+ 32 B slack for 16-byte bulk copies)
+  int64_t nucol = 0;
+  int32_t nlong = 0;           // rows longer than one block (sequential fallback kernel)
+  int32_t* longrows = nullptr;
 };
 
 constexpr int kStreamThreads = 256;

@@ -4,15 +4,22 @@
 // mg.py:41-45 (TransferPair.prolong / restrict — restrict through an explicit
 // transposed CSR), mg.py:270, 294 (residual b - A x).
 //
-// CSR-stream kernel (HBM-bound, 0.17 flop/B): the rows are cut on the host
-// into blocks of <= 2048 nonzeros / 512 rows.  A 256-thread CTA owns one
-// block: every thread issues 8 independent coalesced (col, val) loads plus
-// the 8 x-gathers (x is L2-resident), and stores the products in shared
-// memory; then each row is summed sequentially, left to right, without FMA
-// contraction: y_i = ((0 + a_i0 x_0) + a_i1 x_1) + ...  — the exact
-// operation order of scipy's csr_matvec (and, through the ascending-source
-// transpose, of csc_matvec for masked.T), so SpMV / residual / transfers are
-// bit-identical to the reference.
+// HBM-bound (0.17 flop/B).  Rows are cut on the host into blocks of <= 2048
+// nonzeros / 512 rows, and each block gets a *block-local column
+// compression*: the sorted unique columns it touches plus a 16-bit local
+// index per nonzero (10 instead of 12 streamed bytes per nonzero, and one
+// x-gather per unique column instead of one per nonzero — neighbouring FE
+// rows share most columns).  One 256-thread CTA per block:
+//   * one elected thread issues TMA bulk copies (cp.async.bulk, mbarrier
+//     completion, L2 evict-first) of the block's value and local-index
+//     streams into shared memory;
+//   * meanwhile all threads gather x at the unique columns (L2-resident
+//     vector) into shared memory;
+//   * products are formed in place, then each row is summed sequentially,
+//     left to right, without FMA: y_i = ((0 + a_i0 x_0) + a_i1 x_1) + ... —
+//     the exact operation order of scipy's csr_matvec (and, through the
+//     ascending-source transpose, of csc_matvec for masked.T), so SpMV,
+//     residual and transfers are bit-identical to the reference.
 #include <algorithm>
 #include <cstdarg>
 #include <cstring>
@@ -46,84 +53,131 @@ namespace {
 using vk::kStreamNnz;
 using vk::kStreamRows;
 using vk::kStreamThreads;
-using vk::kStreamU;
+
+// ---- TMA bulk copy / mbarrier helpers (sm_90+ PTX, compiled for sm_100a)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 // MODE 0: y = alpha*Ax + beta*y (beta == 0: y not read);  MODE 1: y = b - A x
 template <int MODE>
-__global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
-    const int* __restrict__ rowblk, const int* __restrict__ ptr, const int* __restrict__ col,
-    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+__device__ __forceinline__ void store_row(int row, double s, double* __restrict__ y, double alpha,
+                                          double beta, const double* __restrict__ b) {
+  if (MODE == 1) {
+    y[row] = __dsub_rn(b[row], s);
+  } else {
+    double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
+    if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[row] : __dmul_rn(beta, y[row]), out);
+    y[row] = out;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kStreamThreads) csr_local_kernel(
+    const int* __restrict__ rowblk, const int* __restrict__ ptr, const double* __restrict__ val,
+    const uint16_t* __restrict__ lidx, const int* __restrict__ ucolptr,
+    const int* __restrict__ ucol, const double* __restrict__ x, double* __restrict__ y,
     double alpha, double beta, const double* __restrict__ b) {
-  __shared__ double prod[kStreamNnz];
+  __shared__ __align__(16) double sval[kStreamNnz + 2];
+  __shared__ __align__(16) uint16_t slid[kStreamNnz + 16];
+  __shared__ double xl[kStreamNnz];
   __shared__ int sptr[kStreamRows + 1];
-  __shared__ double carry;
+  __shared__ __align__(8) uint64_t bar;
   const int t = threadIdx.x;
   const int r0 = rowblk[blockIdx.x], r1 = rowblk[blockIdx.x + 1];
   const int nr = r1 - r0;
-  for (int i = t; i <= nr; i += kStreamThreads) sptr[i] = ptr[r0 + i];
-  __syncthreads();
-  const int k0 = sptr[0], k1 = sptr[nr];
-  const bool single = (nr == 1);
-  if (t == 0) carry = 0.0;
-  for (int kc = k0; kc < k1 || (kc == k0 && k0 == k1); kc += kStreamNnz) {
-    const int kend = min(k1, kc + kStreamNnz);
-    int c[kStreamU];
-    double v[kStreamU];
-#pragma unroll
-    for (int u = 0; u < kStreamU; ++u) {
-      const int k = kc + t + u * kStreamThreads;
-      c[u] = (k < kend) ? __ldcs(col + k) : 0;
-      v[u] = (k < kend) ? __ldcs(val + k) : 0.0;
+  const int k0 = ptr[r0], k1 = ptr[r1];
+  const int nnz = k1 - k0;
+  if (nnz > kStreamNnz) return;    // a single long row: csr_longrow_kernel
+  // 16-byte aligned superset of the block's value / local-index streams
+  const int64_t vb0 = (int64_t(k0) * 8) & ~int64_t(15);
+  const int64_t vb1 = (int64_t(k1) * 8 + 15) & ~int64_t(15);
+  const int64_t lb0 = (int64_t(k0) * 2) & ~int64_t(15);
+  const int64_t lb1 = (int64_t(k1) * 2 + 15) & ~int64_t(15);
+  const int voff = static_cast<int>((int64_t(k0) * 8 - vb0) / 8);
+  const int loff = static_cast<int>((int64_t(k0) * 2 - lb0) / 2);
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    if (nnz > 0) {
+      const uint64_t pol = policy_evict_first();
+      mbar_expect_tx(&bar, static_cast<uint32_t>((vb1 - vb0) + (lb1 - lb0)));
+      bulk_g2s(sval, reinterpret_cast<const char*>(val) + vb0, static_cast<uint32_t>(vb1 - vb0),
+               &bar, pol);
+      bulk_g2s(slid, reinterpret_cast<const char*>(lidx) + lb0, static_cast<uint32_t>(lb1 - lb0),
+               &bar, pol);
     }
-#pragma unroll
-    for (int u = 0; u < kStreamU; ++u) {
-      const int k = kc + t + u * kStreamThreads;
-      if (k < kend) prod[k - kc] = __dmul_rn(v[u], __ldg(x + c[u]));
-    }
-    __syncthreads();
-    if (single) {
-      // a row longer than one chunk: thread 0 carries the sequential sum
-      if (t == 0) {
-        double s = carry;
-        for (int k = kc; k < kend; ++k) s = __dadd_rn(s, prod[k - kc]);
-        carry = s;
-      }
-    } else {
-      for (int i = t; i < nr; i += kStreamThreads) {
-        const int a = sptr[i] - kc, e = sptr[i + 1] - kc;
-        double s = 0.0;
-        for (int k = a; k < e; ++k) s = __dadd_rn(s, prod[k]);
-        const int row = r0 + i;
-        if (MODE == 1) {
-          y[row] = __dsub_rn(b[row], s);
-        } else {
-          double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
-          if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[row] : __dmul_rn(beta, y[row]), out);
-          y[row] = out;
-        }
-      }
-    }
-    __syncthreads();
-    if (k0 == k1) break;
   }
-  if (single && t == 0) {
-    const double s = carry;
-    if (MODE == 1) {
-      y[r0] = __dsub_rn(b[r0], s);
-    } else {
-      double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
-      if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[r0] : __dmul_rn(beta, y[r0]), out);
-      y[r0] = out;
-    }
+  for (int i = t; i <= nr; i += kStreamThreads) sptr[i] = ptr[r0 + i] - k0;
+  const int u0 = ucolptr[blockIdx.x], nu = ucolptr[blockIdx.x + 1] - u0;
+  for (int u = t; u < nu; u += kStreamThreads) xl[u] = __ldg(x + ucol[u0 + u]);
+  __syncthreads();                 // xl, sptr, barrier init visible
+  if (nnz > 0) mbar_wait(&bar, 0);
+  for (int k = t; k < nnz; k += kStreamThreads)
+    sval[voff + k] = __dmul_rn(sval[voff + k], xl[slid[loff + k]]);
+  __syncthreads();
+  const double* prod = sval + voff;
+  for (int i = t; i < nr; i += kStreamThreads) {
+    const int a = sptr[i], e = sptr[i + 1];
+    double s = 0.0;
+    for (int k = a; k < e; ++k) s = __dadd_rn(s, prod[k]);
+    store_row<MODE>(r0 + i, s, y, alpha, beta, b);
+  }
+}
+
+// rows longer than one block (never in the FE operators, kept for generality)
+template <int MODE>
+__global__ void csr_longrow_kernel(const int* __restrict__ rows, int nlong, const int* __restrict__ ptr,
+                                   const int* __restrict__ col, const double* __restrict__ val,
+                                   const double* __restrict__ x, double* __restrict__ y, double alpha,
+                                   double beta, const double* __restrict__ b) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nlong; q += gridDim.x * blockDim.x) {
+    const int row = rows[q];
+    double s = 0.0;
+    for (int k = ptr[row]; k < ptr[row + 1]; ++k) s = __dadd_rn(s, __dmul_rn(val[k], x[col[k]]));
+    store_row<MODE>(row, s, y, alpha, beta, b);
   }
 }
 
 template <int MODE>
 cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alpha, double beta,
                         const double* b, cudaStream_t st) {
-  if (a.nblocks == 0) return cudaSuccess;
-  csr_stream_kernel<MODE><<<a.nblocks, kStreamThreads, 0, st>>>(a.rowblk, a.indptr, a.indices,
-                                                               a.data, x, y, alpha, beta, b);
+  if (a.nblocks > 0)
+    csr_local_kernel<MODE><<<a.nblocks, kStreamThreads, 0, st>>>(
+        a.rowblk, a.indptr, a.data, a.lidx, a.ucolptr, a.ucol, x, y, alpha, beta, b);
+  if (a.nlong > 0)
+    csr_longrow_kernel<MODE><<<std::min((a.nlong + 127) / 128, 148), 128, 0, st>>>(
+        a.longrows, a.nlong, a.indptr, a.indices, a.data, x, y, alpha, beta, b);
   return cudaGetLastError();
 }
 
@@ -139,26 +193,31 @@ __global__ void csr_to_dense_kernel(int nrows, int ncols, const int* __restrict_
   }
 }
 
-// greedy row blocks: <= kStreamNnz nonzeros and <= kStreamRows rows; a row
-// longer than kStreamNnz gets a block of its own
-std::vector<int32_t> make_row_blocks(const std::vector<int32_t>& p) {
+// Row blocks: <= kStreamNnz nonzeros and <= kStreamRows rows.  A row longer
+// than kStreamNnz is diverted to the long-row list.
+void make_row_blocks(const std::vector<int32_t>& p, std::vector<int32_t>& rb,
+                     std::vector<int32_t>& longrows) {
   const int32_t n = static_cast<int32_t>(p.size()) - 1;
-  std::vector<int32_t> rb;
-  rb.push_back(0);
+  rb.assign(1, 0);
   int32_t r = 0;
   while (r < n) {
-    int32_t start = r;
+    const int32_t start = r;
     int64_t nnz = 0;
     while (r < n && r - start < kStreamRows) {
       const int64_t len = p[r + 1] - p[r];
-      if (r > start && nnz + len > kStreamNnz) break;
+      if (len > kStreamNnz) break;
+      if (nnz + len > kStreamNnz) break;
       nnz += len;
       ++r;
-      if (nnz > kStreamNnz) break;  // single long row
+    }
+    if (r == start) {  // a long row: its own block, skipped by the block kernel
+      longrows.push_back(r);
+      ++r;
+      rb.push_back(r);
+      continue;
     }
     rb.push_back(r);
   }
-  return rb;
 }
 
 }  // namespace
@@ -167,36 +226,74 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
                              int32_t nrows, int32_t ncols, int64_t nnz, vk_csr_t* out) {
   VK_REQUIRE(out != nullptr && nrows >= 0 && ncols >= 0 && nnz >= 0, "vk_csr_create: bad args");
   VK_REQUIRE(nnz < (int64_t(1) << 31), "vk_csr_create: nnz exceeds int32 indexing");
-  std::vector<int32_t> hp(nrows + 1);
+  std::vector<int32_t> hp(nrows + 1), hc(nnz);
   cudaError_t e = cudaMemcpy(hp.data(), indptr, sizeof(int32_t) * (nrows + 1), cudaMemcpyDefault);
+  if (e == cudaSuccess && nnz) e = cudaMemcpy(hc.data(), indices, sizeof(int32_t) * nnz, cudaMemcpyDefault);
   if (e != cudaSuccess) {
     vk::set_error("vk_csr_create: %s", cudaGetErrorString(e));
     return VK_ERR_CUDA;
   }
   VK_REQUIRE(hp[0] == 0 && hp[nrows] == nnz, "vk_csr_create: indptr does not match nnz");
-  auto rb = make_row_blocks(hp);
+  for (int32_t i = 0; i < nrows; ++i) {
+    VK_REQUIRE(hp[i + 1] >= hp[i], "vk_csr_create: indptr must be nondecreasing");
+    for (int32_t k = hp[i]; k < hp[i + 1]; ++k)
+      VK_REQUIRE(hc[k] >= 0 && hc[k] < ncols && (k == hp[i] || hc[k] > hc[k - 1]),
+                 "vk_csr_create: row %d column indices must be sorted, unique and in range", i);
+  }
+  std::vector<int32_t> rb, longrows;
+  make_row_blocks(hp, rb, longrows);
+  // block-local column compression
+  const int32_t nb = static_cast<int32_t>(rb.size()) - 1;
+  std::vector<int32_t> up(nb + 1, 0), uc;
+  std::vector<uint16_t> li(nnz + 16, 0);
+  std::vector<int32_t> tmp;
+  for (int32_t bk = 0; bk < nb; ++bk) {
+    const int32_t a = hp[rb[bk]], z = hp[rb[bk + 1]];
+    bool is_long = false;
+    for (int32_t q : longrows)
+      if (q >= rb[bk] && q < rb[bk + 1]) is_long = true;
+    if (!is_long) {
+      tmp.assign(hc.begin() + a, hc.begin() + z);
+      std::sort(tmp.begin(), tmp.end());
+      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+      for (int32_t k = a; k < z; ++k)
+        li[k] = static_cast<uint16_t>(std::lower_bound(tmp.begin(), tmp.end(), hc[k]) - tmp.begin());
+      uc.insert(uc.end(), tmp.begin(), tmp.end());
+    }
+    up[bk + 1] = static_cast<int32_t>(uc.size());
+  }
   auto* a = new vk_csr_s();
   a->nrows = nrows;
   a->ncols = ncols;
   a->nnz = nnz;
-  a->nblocks = static_cast<int32_t>(rb.size()) - 1;
+  a->nblocks = nb;
+  a->nucol = static_cast<int64_t>(uc.size());
+  a->nlong = static_cast<int32_t>(longrows.size());
   e = cudaMalloc(&a->indptr, sizeof(int32_t) * (nrows + 1));
   if (e == cudaSuccess) e = cudaMalloc(&a->indices, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
-  if (e == cudaSuccess) e = cudaMalloc(&a->data, sizeof(double) * std::max<int64_t>(nnz, 1));
+  if (e == cudaSuccess) e = cudaMalloc(&a->data, sizeof(double) * (nnz + 4));
   if (e == cudaSuccess) e = cudaMalloc(&a->rowblk, sizeof(int32_t) * rb.size());
+  if (e == cudaSuccess) e = cudaMalloc(&a->ucolptr, sizeof(int32_t) * up.size());
+  if (e == cudaSuccess) e = cudaMalloc(&a->ucol, sizeof(int32_t) * std::max<size_t>(uc.size(), 1));
+  if (e == cudaSuccess) e = cudaMalloc(&a->lidx, sizeof(uint16_t) * li.size());
+  if (e == cudaSuccess && !longrows.empty())
+    e = cudaMalloc(&a->longrows, sizeof(int32_t) * longrows.size());
   if (e == cudaSuccess)
     e = cudaMemcpy(a->indptr, hp.data(), sizeof(int32_t) * (nrows + 1), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(a->rowblk, rb.data(), sizeof(int32_t) * rb.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(a->ucolptr, up.data(), sizeof(int32_t) * up.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !uc.empty())
+    e = cudaMemcpy(a->ucol, uc.data(), sizeof(int32_t) * uc.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(a->lidx, li.data(), sizeof(uint16_t) * li.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !longrows.empty())
+    e = cudaMemcpy(a->longrows, longrows.data(), sizeof(int32_t) * longrows.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && nnz)
-    e = cudaMemcpy(a->indices, indices, sizeof(int32_t) * nnz, cudaMemcpyDefault);
+    e = cudaMemcpy(a->indices, hc.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && nnz) e = cudaMemcpy(a->data, data, sizeof(double) * nnz, cudaMemcpyDefault);
+  if (e == cudaSuccess) e = cudaMemset(a->data + nnz, 0, sizeof(double) * 4);
   if (e != cudaSuccess) {
     vk::set_error("vk_csr_create: %s", cudaGetErrorString(e));
-    cudaFree(a->indptr);
-    cudaFree(a->indices);
-    cudaFree(a->data);
-    cudaFree(a->rowblk);
-    delete a;
+    vk_csr_destroy(a);
     return VK_ERR_CUDA;
   }
   int32_t mx = 0;
@@ -248,6 +345,10 @@ extern "C" int vk_csr_destroy(vk_csr_t a) {
   cudaFree(a->indices);
   cudaFree(a->data);
   cudaFree(a->rowblk);
+  cudaFree(a->ucolptr);
+  cudaFree(a->ucol);
+  cudaFree(a->lidx);
+  cudaFree(a->longrows);
   delete a;
   return VK_OK;
 }
