@@ -32,6 +32,9 @@ struct Csr {
   int64_t nucol = 0;
   int32_t nlong = 0;           // rows longer than one block (sequential fallback kernel)
   int32_t* longrows = nullptr;
+  int4* blkinfo = nullptr;     // per block {r0, nrows, k0, nnz}
+  int2* blkucol = nullptr;     // per block {u0, nu}
+  int32_t max_nu = 0, max_nr = 0;
 };
 
 constexpr int kStreamThreads = 256;

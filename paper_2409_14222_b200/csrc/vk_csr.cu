@@ -103,55 +103,96 @@ __device__ __forceinline__ void store_row(int row, double s, double* __restrict_
   }
 }
 
+// Persistent, double-buffered pipeline: each CTA walks its row blocks; while
+// block i is reduced, the TMA engine is already fetching block i+1's value,
+// local-index, unique-column and row-pointer streams into the other stage.
+struct StageLayout {
+  int bytes;     // one stage
+  int off_lid, off_ucol, off_ptr;
+  int off_xl;    // after both stages
+};
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(kStreamThreads) csr_local_kernel(
-    const int* __restrict__ rowblk, const int* __restrict__ ptr, const double* __restrict__ val,
-    const uint16_t* __restrict__ lidx, const int* __restrict__ ucolptr,
+__global__ void __launch_bounds__(kStreamThreads) csr_pipe_kernel(
+    int nblk, const int4* __restrict__ info, const int2* __restrict__ uinfo,
+    const int* __restrict__ ptr, const double* __restrict__ val, const uint16_t* __restrict__ lidx,
     const int* __restrict__ ucol, const double* __restrict__ x, double* __restrict__ y,
-    double alpha, double beta, const double* __restrict__ b) {
-  __shared__ __align__(16) double sval[kStreamNnz + 2];
-  __shared__ __align__(16) uint16_t slid[kStreamNnz + 16];
-  __shared__ double xl[kStreamNnz];
-  __shared__ int sptr[kStreamRows + 1];
-  __shared__ __align__(8) uint64_t bar;
+    double alpha, double beta, const double* __restrict__ b, StageLayout L) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[2];
   const int t = threadIdx.x;
-  const int r0 = rowblk[blockIdx.x], r1 = rowblk[blockIdx.x + 1];
-  const int nr = r1 - r0;
-  const int k0 = ptr[r0], k1 = ptr[r1];
-  const int nnz = k1 - k0;
-  if (nnz > kStreamNnz) return;    // a single long row: csr_longrow_kernel
-  // 16-byte aligned superset of the block's value / local-index streams
-  const int64_t vb0 = (int64_t(k0) * 8) & ~int64_t(15);
-  const int64_t vb1 = (int64_t(k1) * 8 + 15) & ~int64_t(15);
-  const int64_t lb0 = (int64_t(k0) * 2) & ~int64_t(15);
-  const int64_t lb1 = (int64_t(k1) * 2 + 15) & ~int64_t(15);
-  const int voff = static_cast<int>((int64_t(k0) * 8 - vb0) / 8);
-  const int loff = static_cast<int>((int64_t(k0) * 2 - lb0) / 2);
-  if (t == 0) {
-    mbar_init(&bar, 1);
-    if (nnz > 0) {
-      const uint64_t pol = policy_evict_first();
-      mbar_expect_tx(&bar, static_cast<uint32_t>((vb1 - vb0) + (lb1 - lb0)));
-      bulk_g2s(sval, reinterpret_cast<const char*>(val) + vb0, static_cast<uint32_t>(vb1 - vb0),
-               &bar, pol);
-      bulk_g2s(slid, reinterpret_cast<const char*>(lidx) + lb0, static_cast<uint32_t>(lb1 - lb0),
-               &bar, pol);
+  double* xl = reinterpret_cast<double*>(smem + L.off_xl);
+
+  // aligned 16-byte superset [lo, hi) of a byte range
+  auto lo16 = [](int64_t v) { return v & ~int64_t(15); };
+  auto hi16 = [](int64_t v) { return (v + 15) & ~int64_t(15); };
+
+  auto issue = [&](int blk, int s) {
+    const int4 in = info[blk];
+    const int2 uu = uinfo[blk];
+    unsigned char* st = smem + s * L.bytes;
+    if (in.w > kStreamNnz || in.w == 0) {
+      mbar_expect_tx(&bar[s], 0);
+      return;
     }
+    const uint64_t pol = policy_evict_first();
+    const int64_t v0 = lo16(int64_t(in.z) * 8), v1 = hi16(int64_t(in.z + in.w) * 8);
+    const int64_t l0 = lo16(int64_t(in.z) * 2), l1 = hi16(int64_t(in.z + in.w) * 2);
+    const int64_t c0 = lo16(int64_t(uu.x) * 4), c1 = hi16(int64_t(uu.x + uu.y) * 4);
+    const int64_t p0 = lo16(int64_t(in.x) * 4), p1 = hi16(int64_t(in.x + in.y + 1) * 4);
+    fence_proxy_async();
+    mbar_expect_tx(&bar[s], static_cast<uint32_t>((v1 - v0) + (l1 - l0) + (c1 - c0) + (p1 - p0)));
+    const uint64_t* dummy = nullptr;
+    (void)dummy;
+    bulk_g2s(st, reinterpret_cast<const char*>(val) + v0, static_cast<uint32_t>(v1 - v0), &bar[s], pol);
+    bulk_g2s(st + L.off_lid, reinterpret_cast<const char*>(lidx) + l0, static_cast<uint32_t>(l1 - l0),
+             &bar[s], pol);
+    if (c1 > c0)
+      bulk_g2s(st + L.off_ucol, reinterpret_cast<const char*>(ucol) + c0, static_cast<uint32_t>(c1 - c0),
+               &bar[s], pol);
+    bulk_g2s(st + L.off_ptr, reinterpret_cast<const char*>(ptr) + p0, static_cast<uint32_t>(p1 - p0),
+             &bar[s], pol);
+  };
+
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
   }
-  for (int i = t; i <= nr; i += kStreamThreads) sptr[i] = ptr[r0 + i] - k0;
-  const int u0 = ucolptr[blockIdx.x], nu = ucolptr[blockIdx.x + 1] - u0;
-  for (int u = t; u < nu; u += kStreamThreads) xl[u] = __ldg(x + ucol[u0 + u]);
-  __syncthreads();                 // xl, sptr, barrier init visible
-  if (nnz > 0) mbar_wait(&bar, 0);
-  for (int k = t; k < nnz; k += kStreamThreads)
-    sval[voff + k] = __dmul_rn(sval[voff + k], xl[slid[loff + k]]);
   __syncthreads();
-  const double* prod = sval + voff;
-  for (int i = t; i < nr; i += kStreamThreads) {
-    const int a = sptr[i], e = sptr[i + 1];
-    double s = 0.0;
-    for (int k = a; k < e; ++k) s = __dadd_rn(s, prod[k]);
-    store_row<MODE>(r0 + i, s, y, alpha, beta, b);
+  if (t == 0 && blockIdx.x < nblk) issue(blockIdx.x, 0);
+  int it = 0;
+  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
+    const int s = it & 1;
+    const int nxt = blk + gridDim.x;
+    if (t == 0 && nxt < nblk) issue(nxt, s ^ 1);
+    const int4 in = info[blk];
+    const int2 uu = uinfo[blk];
+    mbar_wait(&bar[s], (it >> 1) & 1);
+    if (in.w > kStreamNnz) {   // single long row: csr_longrow_kernel
+      __syncthreads();
+      continue;
+    }
+    unsigned char* st = smem + s * L.bytes;
+    const double* sval = reinterpret_cast<const double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
+    double* prod = reinterpret_cast<double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
+    const uint16_t* slid = reinterpret_cast<const uint16_t*>(st + L.off_lid) + ((int64_t(in.z) * 2) & 15) / 2;
+    const int* sucol = reinterpret_cast<const int*>(st + L.off_ucol) + ((int64_t(uu.x) * 4) & 15) / 4;
+    const int* sptr = reinterpret_cast<const int*>(st + L.off_ptr) + ((int64_t(in.x) * 4) & 15) / 4;
+    for (int u = t; u < uu.y; u += kStreamThreads) xl[u] = __ldg(x + sucol[u]);
+    __syncthreads();
+    for (int k = t; k < in.w; k += kStreamThreads) prod[k] = __dmul_rn(sval[k], xl[slid[k]]);
+    __syncthreads();
+    for (int i = t; i < in.y; i += kStreamThreads) {
+      const int a = sptr[i] - in.z, e = sptr[i + 1] - in.z;
+      double sum = 0.0;
+      for (int k = a; k < e; ++k) sum = __dadd_rn(sum, prod[k]);
+      store_row<MODE>(in.x + i, sum, y, alpha, beta, b);
+    }
+    __syncthreads();
   }
 }
 
@@ -169,12 +210,40 @@ __global__ void csr_longrow_kernel(const int* __restrict__ rows, int nlong, cons
   }
 }
 
+void stage_layout(const vk::Csr& a, StageLayout& L) {
+  auto r16 = [](int v) { return (v + 15) & ~15; };
+  const int vbytes = r16(8 * (kStreamNnz + 2));
+  const int lbytes = r16(2 * (kStreamNnz + 16));
+  const int cbytes = r16(4 * (a.max_nu + 8));
+  const int pbytes = r16(4 * (a.max_nr + 1 + 8));
+  L.off_lid = vbytes;
+  L.off_ucol = vbytes + lbytes;
+  L.off_ptr = vbytes + lbytes + cbytes;
+  L.bytes = vbytes + lbytes + cbytes + pbytes;
+  L.off_xl = 2 * L.bytes;
+}
+
 template <int MODE>
 cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alpha, double beta,
                         const double* b, cudaStream_t st) {
-  if (a.nblocks > 0)
-    csr_local_kernel<MODE><<<a.nblocks, kStreamThreads, 0, st>>>(
-        a.rowblk, a.indptr, a.data, a.lidx, a.ucolptr, a.ucol, x, y, alpha, beta, b);
+  if (a.nblocks > 0) {
+    StageLayout L;
+    stage_layout(a, L);
+    const int smem = L.off_xl + 8 * std::max(a.max_nu, 1);
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[MODE]) {
+      cudaFuncSetAttribute(csr_pipe_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           227 * 1024);
+      attr_set[MODE] = true;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_pipe_kernel<MODE>, kStreamThreads, smem);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int grid = std::max(1, std::min(a.nblocks, nsm * std::max(per_sm, 1)));
+    csr_pipe_kernel<MODE><<<grid, kStreamThreads, smem, st>>>(
+        a.nblocks, a.blkinfo, a.blkucol, a.indptr, a.data, a.lidx, a.ucol, x, y, alpha, beta, b, L);
+  }
   if (a.nlong > 0)
     csr_longrow_kernel<MODE><<<std::min((a.nlong + 127) / 128, 148), 128, 0, st>>>(
         a.longrows, a.nlong, a.indptr, a.indices, a.data, x, y, alpha, beta, b);
@@ -249,10 +318,7 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
   std::vector<int32_t> tmp;
   for (int32_t bk = 0; bk < nb; ++bk) {
     const int32_t a = hp[rb[bk]], z = hp[rb[bk + 1]];
-    bool is_long = false;
-    for (int32_t q : longrows)
-      if (q >= rb[bk] && q < rb[bk + 1]) is_long = true;
-    if (!is_long) {
+    if (z - a <= kStreamNnz) {
       tmp.assign(hc.begin() + a, hc.begin() + z);
       std::sort(tmp.begin(), tmp.end());
       tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
@@ -262,6 +328,15 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
     }
     up[bk + 1] = static_cast<int32_t>(uc.size());
   }
+  std::vector<int4> info(std::max(nb, 1));
+  std::vector<int2> uinfo(std::max(nb, 1));
+  int32_t max_nu = 0, max_nr = 0;
+  for (int32_t bk = 0; bk < nb; ++bk) {
+    info[bk] = make_int4(rb[bk], rb[bk + 1] - rb[bk], hp[rb[bk]], hp[rb[bk + 1]] - hp[rb[bk]]);
+    uinfo[bk] = make_int2(up[bk], up[bk + 1] - up[bk]);
+    max_nu = std::max(max_nu, up[bk + 1] - up[bk]);
+    max_nr = std::max(max_nr, rb[bk + 1] - rb[bk]);
+  }
   auto* a = new vk_csr_s();
   a->nrows = nrows;
   a->ncols = ncols;
@@ -269,7 +344,16 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
   a->nblocks = nb;
   a->nucol = static_cast<int64_t>(uc.size());
   a->nlong = static_cast<int32_t>(longrows.size());
-  e = cudaMalloc(&a->indptr, sizeof(int32_t) * (nrows + 1));
+  a->max_nu = max_nu;
+  a->max_nr = max_nr;
+  // +16 B slack on every TMA-streamed array (16-byte aligned superset copies)
+  hp.resize(nrows + 1 + 4, hp[nrows]);
+  uc.resize(uc.size() + 4, 0);
+  e = cudaMalloc(&a->indptr, sizeof(int32_t) * hp.size());
+  if (e == cudaSuccess) e = cudaMalloc(&a->blkinfo, sizeof(int4) * info.size());
+  if (e == cudaSuccess) e = cudaMalloc(&a->blkucol, sizeof(int2) * uinfo.size());
+  if (e == cudaSuccess) e = cudaMemcpy(a->blkinfo, info.data(), sizeof(int4) * info.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(a->blkucol, uinfo.data(), sizeof(int2) * uinfo.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&a->indices, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
   if (e == cudaSuccess) e = cudaMalloc(&a->data, sizeof(double) * (nnz + 4));
   if (e == cudaSuccess) e = cudaMalloc(&a->rowblk, sizeof(int32_t) * rb.size());
@@ -279,7 +363,7 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
   if (e == cudaSuccess && !longrows.empty())
     e = cudaMalloc(&a->longrows, sizeof(int32_t) * longrows.size());
   if (e == cudaSuccess)
-    e = cudaMemcpy(a->indptr, hp.data(), sizeof(int32_t) * (nrows + 1), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(a->indptr, hp.data(), sizeof(int32_t) * hp.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(a->rowblk, rb.data(), sizeof(int32_t) * rb.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(a->ucolptr, up.data(), sizeof(int32_t) * up.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !uc.empty())
@@ -349,6 +433,8 @@ extern "C" int vk_csr_destroy(vk_csr_t a) {
   cudaFree(a->ucol);
   cudaFree(a->lidx);
   cudaFree(a->longrows);
+  cudaFree(a->blkinfo);
+  cudaFree(a->blkucol);
   delete a;
   return VK_OK;
 }
