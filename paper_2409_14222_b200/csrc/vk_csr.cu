@@ -230,11 +230,12 @@ cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alp
     StageLayout L;
     stage_layout(a, L);
     const int smem = L.off_xl + 8 * std::max(a.max_nu, 1);
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[MODE]) {
-      cudaFuncSetAttribute(csr_pipe_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           227 * 1024);
-      attr_set[MODE] = true;
+    static int attr_bytes[2] = {48 * 1024, 48 * 1024};
+    if (smem > attr_bytes[MODE]) {
+      cudaError_t e = cudaFuncSetAttribute(csr_pipe_kernel<MODE>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      attr_bytes[MODE] = smem;
     }
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_pipe_kernel<MODE>, kStreamThreads, smem);
