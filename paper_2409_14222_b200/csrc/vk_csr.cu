@@ -176,6 +176,11 @@ __global__ void __launch_bounds__(kStreamThreads) csr_pipe_kernel(
       __syncthreads();
       continue;
     }
+    if (in.w == 0) {           // only empty rows (e.g. masked BC rows of P): nothing staged
+      for (int i = t; i < in.y; i += kStreamThreads) store_row<MODE>(in.x + i, 0.0, y, alpha, beta, b);
+      __syncthreads();
+      continue;
+    }
     unsigned char* st = smem + s * L.bytes;
     const double* sval = reinterpret_cast<const double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
     double* prod = reinterpret_cast<double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
