@@ -38,9 +38,8 @@ struct Csr {
 };
 
 constexpr int kStreamThreads = 256;
-constexpr int kStreamU = 8;
-constexpr int kStreamNnz = kStreamThreads * kStreamU;   // 2048 nonzeros per block
-constexpr int kStreamRows = 512;
+constexpr int kStreamNnz = 2040;   // nonzeros per row block (<= 256 aligned groups of 8)
+constexpr int kStreamRows = 512;   // rows per row block
 
 // Patch set: CSR-like layout of patch DoF lists + explicit inverses.
 struct Patches {

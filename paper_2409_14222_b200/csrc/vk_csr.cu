@@ -4,22 +4,19 @@
 // mg.py:41-45 (TransferPair.prolong / restrict — restrict through an explicit
 // transposed CSR), mg.py:270, 294 (residual b - A x).
 //
-// HBM-bound (0.17 flop/B).  Rows are cut on the host into blocks of <= 2048
+// HBM-bound (0.17 flop/B).  Rows are cut on the host into blocks of <= 2040
 // nonzeros / 512 rows, and each block gets a *block-local column
 // compression*: the sorted unique columns it touches plus a 16-bit local
 // index per nonzero (10 instead of 12 streamed bytes per nonzero, and one
 // x-gather per unique column instead of one per nonzero — neighbouring FE
-// rows share most columns).  One 256-thread CTA per block:
-//   * one elected thread issues TMA bulk copies (cp.async.bulk, mbarrier
-//     completion, L2 evict-first) of the block's value and local-index
-//     streams into shared memory;
-//   * meanwhile all threads gather x at the unique columns (L2-resident
-//     vector) into shared memory;
-//   * products are formed in place, then each row is summed sequentially,
-//     left to right, without FMA: y_i = ((0 + a_i0 x_0) + a_i1 x_1) + ... —
-//     the exact operation order of scipy's csr_matvec (and, through the
-//     ascending-source transpose, of csc_matvec for masked.T), so SpMV,
-//     residual and transfers are bit-identical to the reference.
+// rows share most columns).  Persistent CTAs stream the blocks through a
+// three-deep register pipeline (128-bit value / index loads of block i+2,
+// x gathers of block i+1, row sums of block i), see csr_pipe_kernel.  Each
+// row is summed sequentially, left to right, without FMA:
+// y_i = ((0 + a_i0 x_0) + a_i1 x_1) + ... — the exact operation order of
+// scipy's csr_matvec (and, through the ascending-source transpose, of
+// csc_matvec for masked.T), so SpMV, residual and transfers are
+// bit-identical to the reference.
 #include <algorithm>
 #include <cstdarg>
 #include <cstring>
@@ -54,42 +51,6 @@ using vk::kStreamNnz;
 using vk::kStreamRows;
 using vk::kStreamThreads;
 
-// ---- TMA bulk copy / mbarrier helpers (sm_90+ PTX, compiled for sm_100a)
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
 // MODE 0: y = alpha*Ax + beta*y (beta == 0: y not read);  MODE 1: y = b - A x
 template <int MODE>
 __device__ __forceinline__ void store_row(int row, double s, double* __restrict__ y, double alpha,
@@ -103,101 +64,135 @@ __device__ __forceinline__ void store_row(int row, double s, double* __restrict_
   }
 }
 
-// Persistent, double-buffered pipeline: each CTA walks its row blocks; while
-// block i is reduced, the TMA engine is already fetching block i+1's value,
-// local-index, unique-column and row-pointer streams into the other stage.
-struct StageLayout {
-  int bytes;     // one stage
-  int off_lid, off_ucol, off_ptr;
-  int off_xl;    // after both stages
+constexpr int kMaxU = 8;   // unique columns per thread: nu <= 2048
+
+// One row block ("chunk") held in registers while it is in flight.  Thread t
+// owns the 16-byte-aligned group of 8 nonzeros starting at (k0 & ~7) + 8t:
+// one 128-bit load of local indices and four 128-bit loads of values.
+struct ChunkRegs {
+  int4 info;           // r0, nrows, k0, nnz   (nnz = 0: no chunk)
+  int2 uu;             // u0, nu
+  uint4 lid;
+  double2 v[4];
+  int uc[kMaxU];
+  int p0, p1;          // row pointers of rows t and t + 256
 };
 
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+__device__ __forceinline__ void load_chunk(int blk, int nblk, ChunkRegs& c, const int4* __restrict__ info,
+                                           const int2* __restrict__ uinfo, const int* __restrict__ ptr,
+                                           const double* __restrict__ val,
+                                           const uint16_t* __restrict__ lidx,
+                                           const int* __restrict__ ucol) {
+  const int t = threadIdx.x;
+  if (blk >= nblk) {
+    c.info = make_int4(0, 0, 0, 0);
+    c.uu = make_int2(0, 0);
+    return;
+  }
+  c.info = __ldg(info + blk);
+  c.uu = __ldg(uinfo + blk);
+  const int k0 = c.info.z, nnz = c.info.w;
+  if (nnz > kStreamNnz) {      // a single long row: csr_longrow_kernel
+    c.info.w = 0;
+    c.info.y = 0;
+    c.uu.y = 0;
+    return;
+  }
+  const int e = (k0 & ~7) + 8 * t;
+  if (e < k0 + nnz) {
+    c.lid = __ldcs(reinterpret_cast<const uint4*>(lidx + e));
+    const double2* vp = reinterpret_cast<const double2*>(val + e);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c.v[q] = __ldcs(vp + q);
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxU; ++j) {
+    const int u = t + kStreamThreads * j;
+    c.uc[j] = (u < c.uu.y) ? __ldg(ucol + c.uu.x + u) : 0;
+  }
+  c.p0 = (t <= c.info.y) ? __ldg(ptr + c.info.x + t) : 0;
+  c.p1 = (t + kStreamThreads <= c.info.y) ? __ldg(ptr + c.info.x + t + kStreamThreads) : 0;
 }
 
+__device__ __forceinline__ int lid_of(const uint4& l, int j) {
+  const unsigned w = (j < 2) ? l.x : (j < 4) ? l.y : (j < 6) ? l.z : l.w;
+  return (j & 1) ? int(w >> 16) : int(w & 0xffffu);
+}
+
+// Persistent CTAs walk their row blocks with a register-level software
+// pipeline, three chunks deep: in one iteration a CTA
+//   (1) issues the x gathers (unique columns, L2) of chunk i+1,
+//   (2) issues the 128-bit value / local-index loads (HBM) of chunk i+2,
+//   (3) sums the rows of chunk i sequentially out of shared memory,
+//   (4) stages chunk i+1's x values and row pointers, then forms its products.
+// Memory latency of (1) and (2) hides behind (3); no TMA engine or async
+// barrier is needed because every stream is a plain coalesced load.
 template <int MODE>
-__global__ void __launch_bounds__(kStreamThreads) csr_pipe_kernel(
+__global__ void __launch_bounds__(kStreamThreads, 2) csr_pipe_kernel(
     int nblk, const int4* __restrict__ info, const int2* __restrict__ uinfo,
     const int* __restrict__ ptr, const double* __restrict__ val, const uint16_t* __restrict__ lidx,
     const int* __restrict__ ucol, const double* __restrict__ x, double* __restrict__ y,
-    double alpha, double beta, const double* __restrict__ b, StageLayout L) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[2];
+    double alpha, double beta, const double* __restrict__ b) {
+  extern __shared__ __align__(16) double dsm[];
+  double(*prod)[kStreamNnz + 8] = reinterpret_cast<double(*)[kStreamNnz + 8]>(dsm);
+  double* xl = dsm + 2 * (kStreamNnz + 8);
+  int(*sptr)[kStreamRows + 1] =
+      reinterpret_cast<int(*)[kStreamRows + 1]>(xl + kStreamThreads * kMaxU);
   const int t = threadIdx.x;
-  double* xl = reinterpret_cast<double*>(smem + L.off_xl);
-
-  // aligned 16-byte superset [lo, hi) of a byte range
-  auto lo16 = [](int64_t v) { return v & ~int64_t(15); };
-  auto hi16 = [](int64_t v) { return (v + 15) & ~int64_t(15); };
-
-  auto issue = [&](int blk, int s) {
-    const int4 in = info[blk];
-    const int2 uu = uinfo[blk];
-    unsigned char* st = smem + s * L.bytes;
-    if (in.w > kStreamNnz || in.w == 0) {
-      mbar_expect_tx(&bar[s], 0);
-      return;
+  const int G = gridDim.x;
+  ChunkRegs nxt, aft;
+  load_chunk(blockIdx.x, nblk, nxt, info, uinfo, ptr, val, lidx, ucol);
+  for (int it = 0;; ++it) {
+    const int blk_next = blockIdx.x + it * G;       // produced this iteration
+    const int blk_cur = blk_next - G;               // reduced this iteration
+    if (blk_cur >= nblk) break;
+    // (1) x gathers of the next chunk
+    double xv[kMaxU];
+#pragma unroll
+    for (int j = 0; j < kMaxU; ++j) {
+      const int u = t + kStreamThreads * j;
+      xv[j] = (u < nxt.uu.y) ? __ldg(x + nxt.uc[j]) : 0.0;
     }
-    const uint64_t pol = policy_evict_first();
-    const int64_t v0 = lo16(int64_t(in.z) * 8), v1 = hi16(int64_t(in.z + in.w) * 8);
-    const int64_t l0 = lo16(int64_t(in.z) * 2), l1 = hi16(int64_t(in.z + in.w) * 2);
-    const int64_t c0 = lo16(int64_t(uu.x) * 4), c1 = hi16(int64_t(uu.x + uu.y) * 4);
-    const int64_t p0 = lo16(int64_t(in.x) * 4), p1 = hi16(int64_t(in.x + in.y + 1) * 4);
-    fence_proxy_async();
-    mbar_expect_tx(&bar[s], static_cast<uint32_t>((v1 - v0) + (l1 - l0) + (c1 - c0) + (p1 - p0)));
-    const uint64_t* dummy = nullptr;
-    (void)dummy;
-    bulk_g2s(st, reinterpret_cast<const char*>(val) + v0, static_cast<uint32_t>(v1 - v0), &bar[s], pol);
-    bulk_g2s(st + L.off_lid, reinterpret_cast<const char*>(lidx) + l0, static_cast<uint32_t>(l1 - l0),
-             &bar[s], pol);
-    if (c1 > c0)
-      bulk_g2s(st + L.off_ucol, reinterpret_cast<const char*>(ucol) + c0, static_cast<uint32_t>(c1 - c0),
-               &bar[s], pol);
-    bulk_g2s(st + L.off_ptr, reinterpret_cast<const char*>(ptr) + p0, static_cast<uint32_t>(p1 - p0),
-             &bar[s], pol);
-  };
-
-  if (t == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-  }
-  __syncthreads();
-  if (t == 0 && blockIdx.x < nblk) issue(blockIdx.x, 0);
-  int it = 0;
-  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
+    // (2) streams of the chunk after next
+    load_chunk(blk_next + G, nblk, aft, info, uinfo, ptr, val, lidx, ucol);
+    // (3) sequential, FMA-free row sums of the current chunk (scipy order)
+    if (it > 0 && blk_cur < nblk) {
+      const int4 ci = __ldg(info + blk_cur);
+      if (ci.w <= kStreamNnz) {
+        const int s = (it - 1) & 1;
+        const double* pr = prod[s];
+        for (int i = t; i < ci.y; i += kStreamThreads) {
+          const int a = sptr[s][i] - ci.z, e = sptr[s][i + 1] - ci.z;
+          double sum = 0.0;
+          for (int k = a; k < e; ++k) sum = __dadd_rn(sum, pr[k]);
+          store_row<MODE>(ci.x + i, sum, y, alpha, beta, b);
+        }
+      }
+    }
+    // (4) stage x and row pointers of the next chunk, then its products
     const int s = it & 1;
-    const int nxt = blk + gridDim.x;
-    if (t == 0 && nxt < nblk) issue(nxt, s ^ 1);
-    const int4 in = info[blk];
-    const int2 uu = uinfo[blk];
-    mbar_wait(&bar[s], (it >> 1) & 1);
-    if (in.w > kStreamNnz) {   // single long row: csr_longrow_kernel
-      __syncthreads();
-      continue;
+#pragma unroll
+    for (int j = 0; j < kMaxU; ++j) {
+      const int u = t + kStreamThreads * j;
+      if (u < nxt.uu.y) xl[u] = xv[j];
     }
-    if (in.w == 0) {           // only empty rows (e.g. masked BC rows of P): nothing staged
-      for (int i = t; i < in.y; i += kStreamThreads) store_row<MODE>(in.x + i, 0.0, y, alpha, beta, b);
-      __syncthreads();
-      continue;
-    }
-    unsigned char* st = smem + s * L.bytes;
-    const double* sval = reinterpret_cast<const double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
-    double* prod = reinterpret_cast<double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
-    const uint16_t* slid = reinterpret_cast<const uint16_t*>(st + L.off_lid) + ((int64_t(in.z) * 2) & 15) / 2;
-    const int* sucol = reinterpret_cast<const int*>(st + L.off_ucol) + ((int64_t(uu.x) * 4) & 15) / 4;
-    const int* sptr = reinterpret_cast<const int*>(st + L.off_ptr) + ((int64_t(in.x) * 4) & 15) / 4;
-    for (int u = t; u < uu.y; u += kStreamThreads) xl[u] = __ldg(x + sucol[u]);
+    if (t <= nxt.info.y) sptr[s][t] = nxt.p0;
+    if (t + kStreamThreads <= nxt.info.y) sptr[s][t + kStreamThreads] = nxt.p1;
     __syncthreads();
-    for (int k = t; k < in.w; k += kStreamThreads) prod[k] = __dmul_rn(sval[k], xl[slid[k]]);
-    __syncthreads();
-    for (int i = t; i < in.y; i += kStreamThreads) {
-      const int a = sptr[i] - in.z, e = sptr[i + 1] - in.z;
-      double sum = 0.0;
-      for (int k = a; k < e; ++k) sum = __dadd_rn(sum, prod[k]);
-      store_row<MODE>(in.x + i, sum, y, alpha, beta, b);
+    if (nxt.info.w > 0) {
+      const int k0 = nxt.info.z;
+      const int e = (k0 & ~7) + 8 * t;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = e + j - k0;
+        if (k >= 0 && k < nxt.info.w) {
+          const double vj = (j & 1) ? nxt.v[j >> 1].y : nxt.v[j >> 1].x;
+          prod[s][k] = __dmul_rn(vj, xl[lid_of(nxt.lid, j)]);
+        }
+      }
     }
     __syncthreads();
+    nxt = aft;
   }
 }
 
@@ -215,40 +210,26 @@ __global__ void csr_longrow_kernel(const int* __restrict__ rows, int nlong, cons
   }
 }
 
-void stage_layout(const vk::Csr& a, StageLayout& L) {
-  auto r16 = [](int v) { return (v + 15) & ~15; };
-  const int vbytes = r16(8 * (kStreamNnz + 2));
-  const int lbytes = r16(2 * (kStreamNnz + 16));
-  const int cbytes = r16(4 * (a.max_nu + 8));
-  const int pbytes = r16(4 * (a.max_nr + 1 + 8));
-  L.off_lid = vbytes;
-  L.off_ucol = vbytes + lbytes;
-  L.off_ptr = vbytes + lbytes + cbytes;
-  L.bytes = vbytes + lbytes + cbytes + pbytes;
-  L.off_xl = 2 * L.bytes;
-}
-
 template <int MODE>
 cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alpha, double beta,
                         const double* b, cudaStream_t st) {
   if (a.nblocks > 0) {
-    StageLayout L;
-    stage_layout(a, L);
-    const int smem = L.off_xl + 8 * std::max(a.max_nu, 1);
-    static int attr_bytes[2] = {48 * 1024, 48 * 1024};
-    if (smem > attr_bytes[MODE]) {
+    const int smem = static_cast<int>(sizeof(double) * (2 * (kStreamNnz + 8) + kStreamThreads * kMaxU) +
+                                      sizeof(int) * 2 * (kStreamRows + 1));
+    static bool attr[2] = {false, false};
+    if (!attr[MODE]) {
       cudaError_t e = cudaFuncSetAttribute(csr_pipe_kernel<MODE>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
-      attr_bytes[MODE] = smem;
+      attr[MODE] = true;
     }
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_pipe_kernel<MODE>, kStreamThreads, smem);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     const int grid = std::max(1, std::min(a.nblocks, nsm * std::max(per_sm, 1)));
-    csr_pipe_kernel<MODE><<<grid, kStreamThreads, smem, st>>>(
-        a.nblocks, a.blkinfo, a.blkucol, a.indptr, a.data, a.lidx, a.ucol, x, y, alpha, beta, b, L);
+    csr_pipe_kernel<MODE><<<grid, kStreamThreads, smem, st>>>(a.nblocks, a.blkinfo, a.blkucol, a.indptr,
+                                                           a.data, a.lidx, a.ucol, x, y, alpha, beta, b);
   }
   if (a.nlong > 0)
     csr_longrow_kernel<MODE><<<std::min((a.nlong + 127) / 128, 148), 128, 0, st>>>(
@@ -361,7 +342,7 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
   if (e == cudaSuccess) e = cudaMemcpy(a->blkinfo, info.data(), sizeof(int4) * info.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(a->blkucol, uinfo.data(), sizeof(int2) * uinfo.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&a->indices, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
-  if (e == cudaSuccess) e = cudaMalloc(&a->data, sizeof(double) * (nnz + 4));
+  if (e == cudaSuccess) e = cudaMalloc(&a->data, sizeof(double) * (nnz + 8));
   if (e == cudaSuccess) e = cudaMalloc(&a->rowblk, sizeof(int32_t) * rb.size());
   if (e == cudaSuccess) e = cudaMalloc(&a->ucolptr, sizeof(int32_t) * up.size());
   if (e == cudaSuccess) e = cudaMalloc(&a->ucol, sizeof(int32_t) * std::max<size_t>(uc.size(), 1));
@@ -380,7 +361,7 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
   if (e == cudaSuccess && nnz)
     e = cudaMemcpy(a->indices, hc.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && nnz) e = cudaMemcpy(a->data, data, sizeof(double) * nnz, cudaMemcpyDefault);
-  if (e == cudaSuccess) e = cudaMemset(a->data + nnz, 0, sizeof(double) * 4);
+  if (e == cudaSuccess) e = cudaMemset(a->data + nnz, 0, sizeof(double) * 8);
   if (e != cudaSuccess) {
     vk::set_error("vk_csr_create: %s", cudaGetErrorString(e));
     vk_csr_destroy(a);
