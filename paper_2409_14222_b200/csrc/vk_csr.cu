@@ -259,7 +259,8 @@ void make_row_blocks(const std::vector<int32_t>& p, std::vector<int32_t>& rb,
   while (r < n) {
     const int32_t start = r;
     int64_t nnz = 0;
-    while (r < n && r - start < kStreamRows - 1)  // <= 511 rows: 512 row pointers = 2 per thread {
+    // <= 511 rows: the 512 row pointers of a block are two per thread
+    while (r < n && r - start < kStreamRows - 1) {
       const int64_t len = p[r + 1] - p[r];
       if (len > kStreamNnz) break;
       if (nnz + len > kStreamNnz) break;
