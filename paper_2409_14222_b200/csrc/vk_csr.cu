@@ -5,13 +5,12 @@
 // transposed CSR), mg.py:270, 294 (residual b - A x).
 //
 // HBM-bound (0.17 flop/B).  Rows are cut on the host into blocks of <= 2040
-// nonzeros / 512 rows, and each block gets a *block-local column
+// nonzeros / 511 rows, and each block gets a *block-local column
 // compression*: the sorted unique columns it touches plus a 16-bit local
 // index per nonzero (10 instead of 12 streamed bytes per nonzero, and one
 // x-gather per unique column instead of one per nonzero — neighbouring FE
-// rows share most columns).  Persistent CTAs stream the blocks through a
-// three-deep register pipeline (128-bit value / index loads of block i+2,
-// x gathers of block i+1, row sums of block i), see csr_pipe_kernel.  Each
+// rows share most columns).  A warp-specialised persistent kernel streams the
+// blocks through a TMA ring (csr_ws_kernel).  Each
 // row is summed sequentially, left to right, without FMA:
 // y_i = ((0 + a_i0 x_0) + a_i1 x_1) + ... — the exact operation order of
 // scipy's csr_matvec (and, through the ascending-source transpose, of
@@ -64,135 +63,178 @@ __device__ __forceinline__ void store_row(int row, double s, double* __restrict_
   }
 }
 
-constexpr int kMaxU = 8;   // unique columns per thread: nu <= 2048
+// ---- TMA bulk copy / mbarrier helpers (PTX, sm_90+; compiled for sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 
-// One row block ("chunk") held in registers while it is in flight.  Thread t
-// owns the 16-byte-aligned group of 8 nonzeros starting at (k0 & ~7) + 8t:
-// one 128-bit load of local indices and four 128-bit loads of values.
-struct ChunkRegs {
-  int4 info;           // r0, nrows, k0, nnz   (nnz = 0: no chunk)
-  int2 uu;             // u0, nu
-  uint4 lid;
-  double2 v[4];
-  int uc[kMaxU];
-  int p0, p1;          // row pointers of rows t and t + 256
+// Warp-specialised, persistent CSR kernel (one CTA per SM):
+//   warp 0        : one elected thread streams each row block's value,
+//                   local-index, unique-column and row-pointer ranges into a
+//                   kStages-deep shared-memory ring with cp.async.bulk (TMA),
+//                   completion on a per-stage mbarrier;
+//   warps 1..8    : product warps — gather x at the block's unique columns
+//                   (L2) into a double-buffered table, then form the products
+//                   a_k * x_col(k) in place of the staged values;
+//   warps 9..11   : consumer warps — sum each row sequentially, left to right,
+//                   without FMA (scipy's order), apply the epilogue, release
+//                   the stage.
+// TMA, gathers and the serial row sums of different blocks overlap, which a
+// bulk-synchronous CTA cannot do (the row sums are a dependency chain).
+constexpr int kStages = 4;
+constexpr int kProdWarps = 8;
+constexpr int kConsWarps = 3;
+constexpr int kPipeThreads = 32 * (1 + kProdWarps + kConsWarps);   // 384
+
+struct PipeLayout {
+  int stage_bytes, off_lid, off_ucol, off_ptr, off_xl, xl_doubles;
 };
 
-__device__ __forceinline__ void load_chunk(int blk, int nblk, ChunkRegs& c, const int4* __restrict__ info,
-                                           const int2* __restrict__ uinfo, const int* __restrict__ ptr,
-                                           const double* __restrict__ val,
-                                           const uint16_t* __restrict__ lidx,
-                                           const int* __restrict__ ucol) {
-  const int t = threadIdx.x;
-  if (blk >= nblk) {
-    c.info = make_int4(0, 0, 0, 0);
-    c.uu = make_int2(0, 0);
-    return;
-  }
-  c.info = __ldg(info + blk);
-  c.uu = __ldg(uinfo + blk);
-  const int k0 = c.info.z, nnz = c.info.w;
-  if (nnz > kStreamNnz) {      // a single long row: csr_longrow_kernel
-    c.info.w = 0;
-    c.info.y = 0;
-    c.uu.y = 0;
-    return;
-  }
-  const int e = (k0 & ~7) + 8 * t;
-  if (e < k0 + nnz) {
-    c.lid = __ldcs(reinterpret_cast<const uint4*>(lidx + e));
-    const double2* vp = reinterpret_cast<const double2*>(val + e);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) c.v[q] = __ldcs(vp + q);
-  }
-#pragma unroll
-  for (int j = 0; j < kMaxU; ++j) {
-    const int u = t + kStreamThreads * j;
-    c.uc[j] = (u < c.uu.y) ? __ldg(ucol + c.uu.x + u) : 0;
-  }
-  c.p0 = (t <= c.info.y) ? __ldg(ptr + c.info.x + t) : 0;
-  c.p1 = (t + kStreamThreads <= c.info.y) ? __ldg(ptr + c.info.x + t + kStreamThreads) : 0;
-}
-
-__device__ __forceinline__ int lid_of(const uint4& l, int j) {
-  const unsigned w = (j < 2) ? l.x : (j < 4) ? l.y : (j < 6) ? l.z : l.w;
-  return (j & 1) ? int(w >> 16) : int(w & 0xffffu);
-}
-
-// Persistent CTAs walk their row blocks with a register-level software
-// pipeline, three chunks deep: in one iteration a CTA
-//   (1) issues the x gathers (unique columns, L2) of chunk i+1,
-//   (2) issues the 128-bit value / local-index loads (HBM) of chunk i+2,
-//   (3) sums the rows of chunk i sequentially out of shared memory,
-//   (4) stages chunk i+1's x values and row pointers, then forms its products.
-// Memory latency of (1) and (2) hides behind (3); no TMA engine or async
-// barrier is needed because every stream is a plain coalesced load.
 template <int MODE>
-__global__ void __launch_bounds__(kStreamThreads, 2) csr_pipe_kernel(
+__global__ void __launch_bounds__(kPipeThreads, 1) csr_ws_kernel(
     int nblk, const int4* __restrict__ info, const int2* __restrict__ uinfo,
     const int* __restrict__ ptr, const double* __restrict__ val, const uint16_t* __restrict__ lidx,
     const int* __restrict__ ucol, const double* __restrict__ x, double* __restrict__ y,
-    double alpha, double beta, const double* __restrict__ b) {
-  extern __shared__ __align__(16) double dsm[];
-  double(*prod)[kStreamNnz + 8] = reinterpret_cast<double(*)[kStreamNnz + 8]>(dsm);
-  double* xl = dsm + 2 * (kStreamNnz + 8);
-  int(*sptr)[kStreamRows + 1] =
-      reinterpret_cast<int(*)[kStreamRows + 1]>(xl + kStreamThreads * kMaxU);
-  const int t = threadIdx.x;
+    double alpha, double beta, const double* __restrict__ b, PipeLayout L) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full_bar[kStages], prod_bar[kStages], empty_bar[kStages];
+  const int warp = threadIdx.x >> 5;
   const int G = gridDim.x;
-  ChunkRegs nxt, aft;
-  load_chunk(blockIdx.x, nblk, nxt, info, uinfo, ptr, val, lidx, ucol);
-  for (int it = 0;; ++it) {
-    const int blk_next = blockIdx.x + it * G;       // produced this iteration
-    const int blk_cur = blk_next - G;               // reduced this iteration
-    if (blk_cur >= nblk) break;
-    // (1) x gathers of the next chunk
-    double xv[kMaxU];
-#pragma unroll
-    for (int j = 0; j < kMaxU; ++j) {
-      const int u = t + kStreamThreads * j;
-      xv[j] = (u < nxt.uu.y) ? __ldg(x + nxt.uc[j]) : 0.0;
+  auto lo16 = [](int64_t v) { return v & ~int64_t(15); };
+  auto hi16 = [](int64_t v) { return (v + 15) & ~int64_t(15); };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&prod_bar[s], 32 * kProdWarps);
+      mbar_init(&empty_bar[s], 32 * kConsWarps);
     }
-    // (2) streams of the chunk after next
-    load_chunk(blk_next + G, nblk, aft, info, uinfo, ptr, val, lidx, ucol);
-    // (3) sequential, FMA-free row sums of the current chunk (scipy order)
-    if (it > 0 && blk_cur < nblk) {
-      const int4 ci = __ldg(info + blk_cur);
-      if (ci.w <= kStreamNnz) {
-        const int s = (it - 1) & 1;
-        const double* pr = prod[s];
-        for (int i = t; i < ci.y; i += kStreamThreads) {
-          const int a = sptr[s][i] - ci.z, e = sptr[s][i + 1] - ci.z;
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (threadIdx.x == 0) {
+      const uint64_t pol = policy_evict_first();
+      int c = 0;
+      for (int blk = blockIdx.x; blk < nblk; blk += G, ++c) {
+        const int s = c % kStages;
+        if (c >= kStages) mbar_wait(&empty_bar[s], ((c / kStages) - 1) & 1);
+        const int4 in = __ldg(info + blk);
+        const int2 uu = __ldg(uinfo + blk);
+        unsigned char* st = smem + s * L.stage_bytes;
+        if (in.w == 0 || in.w > kStreamNnz) {
+          mbar_expect_tx(&full_bar[s], 0);
+          continue;
+        }
+        const int64_t v0 = lo16(int64_t(in.z) * 8), v1 = hi16(int64_t(in.z + in.w) * 8);
+        const int64_t l0 = lo16(int64_t(in.z) * 2), l1 = hi16(int64_t(in.z + in.w) * 2);
+        const int64_t c0 = lo16(int64_t(uu.x) * 4), c1 = hi16(int64_t(uu.x + uu.y) * 4);
+        const int64_t p0 = lo16(int64_t(in.x) * 4), p1 = hi16(int64_t(in.x + in.y + 1) * 4);
+        fence_proxy_async();
+        mbar_expect_tx(&full_bar[s],
+                       static_cast<uint32_t>((v1 - v0) + (l1 - l0) + (c1 - c0) + (p1 - p0)));
+        bulk_g2s(st, reinterpret_cast<const char*>(val) + v0, uint32_t(v1 - v0), &full_bar[s], pol);
+        bulk_g2s(st + L.off_lid, reinterpret_cast<const char*>(lidx) + l0, uint32_t(l1 - l0),
+                 &full_bar[s], pol);
+        if (c1 > c0)
+          bulk_g2s(st + L.off_ucol, reinterpret_cast<const char*>(ucol) + c0, uint32_t(c1 - c0),
+                   &full_bar[s], pol);
+        bulk_g2s(st + L.off_ptr, reinterpret_cast<const char*>(ptr) + p0, uint32_t(p1 - p0),
+                 &full_bar[s], pol);
+      }
+    }
+  } else if (warp <= kProdWarps) {
+    // ------------------------------------------------------ product warps
+    const int t = threadIdx.x - 32;
+    constexpr int NT = 32 * kProdWarps;
+    int c = 0;
+    for (int blk = blockIdx.x; blk < nblk; blk += G, ++c) {
+      const int s = c % kStages;
+      mbar_wait(&full_bar[s], (c / kStages) & 1);
+      const int4 in = __ldg(info + blk);
+      const int2 uu = __ldg(uinfo + blk);
+      const bool live = in.w > 0 && in.w <= kStreamNnz;
+      unsigned char* st = smem + s * L.stage_bytes;
+      double* xl = reinterpret_cast<double*>(smem + L.off_xl) + (c & 1) * L.xl_doubles;
+      if (live) {
+        const int* sucol = reinterpret_cast<const int*>(st + L.off_ucol) + ((int64_t(uu.x) * 4) & 15) / 4;
+        for (int u = t; u < uu.y; u += NT) xl[u] = __ldg(x + sucol[u]);
+      }
+      named_bar_sync(1, NT);   // every chunk: also orders xl[c&1] reuse two chunks later
+      if (live) {
+        double* sv = reinterpret_cast<double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
+        const uint16_t* sl = reinterpret_cast<const uint16_t*>(st + L.off_lid) + ((int64_t(in.z) * 2) & 15) / 2;
+        for (int k = t; k < in.w; k += NT) sv[k] = __dmul_rn(sv[k], xl[sl[k]]);
+      }
+      mbar_arrive(&prod_bar[s]);
+    }
+  } else {
+    // ------------------------------------------------------ consumer warps
+    const int t = threadIdx.x - 32 * (1 + kProdWarps);
+    constexpr int NT = 32 * kConsWarps;
+    int c = 0;
+    for (int blk = blockIdx.x; blk < nblk; blk += G, ++c) {
+      const int s = c % kStages;
+      mbar_wait(&prod_bar[s], (c / kStages) & 1);
+      const int4 in = __ldg(info + blk);
+      if (in.w <= kStreamNnz) {
+        unsigned char* st = smem + s * L.stage_bytes;
+        const double* pr = reinterpret_cast<const double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
+        const int* sp = reinterpret_cast<const int*>(st + L.off_ptr) + ((int64_t(in.x) * 4) & 15) / 4;
+        for (int i = t; i < in.y; i += NT) {
           double sum = 0.0;
-          for (int k = a; k < e; ++k) sum = __dadd_rn(sum, pr[k]);
-          store_row<MODE>(ci.x + i, sum, y, alpha, beta, b);
+          if (in.w > 0) {
+            const int a = sp[i] - in.z, e = sp[i + 1] - in.z;
+            for (int k = a; k < e; ++k) sum = __dadd_rn(sum, pr[k]);
+          }
+          store_row<MODE>(in.x + i, sum, y, alpha, beta, b);
         }
       }
+      mbar_arrive(&empty_bar[s]);
     }
-    // (4) stage x and row pointers of the next chunk, then its products
-    const int s = it & 1;
-#pragma unroll
-    for (int j = 0; j < kMaxU; ++j) {
-      const int u = t + kStreamThreads * j;
-      if (u < nxt.uu.y) xl[u] = xv[j];
-    }
-    if (t <= nxt.info.y) sptr[s][t] = nxt.p0;
-    if (t + kStreamThreads <= nxt.info.y) sptr[s][t + kStreamThreads] = nxt.p1;
-    __syncthreads();
-    if (nxt.info.w > 0) {
-      const int k0 = nxt.info.z;
-      const int e = (k0 & ~7) + 8 * t;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int k = e + j - k0;
-        if (k >= 0 && k < nxt.info.w) {
-          const double vj = (j & 1) ? nxt.v[j >> 1].y : nxt.v[j >> 1].x;
-          prod[s][k] = __dmul_rn(vj, xl[lid_of(nxt.lid, j)]);
-        }
-      }
-    }
-    __syncthreads();
-    nxt = aft;
   }
 }
 
@@ -214,22 +256,32 @@ template <int MODE>
 cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alpha, double beta,
                         const double* b, cudaStream_t st) {
   if (a.nblocks > 0) {
-    const int smem = static_cast<int>(sizeof(double) * (2 * (kStreamNnz + 8) + kStreamThreads * kMaxU) +
-                                      sizeof(int) * 2 * (kStreamRows + 1));
-    static bool attr[2] = {false, false};
-    if (!attr[MODE]) {
-      cudaError_t e = cudaFuncSetAttribute(csr_pipe_kernel<MODE>,
+    auto r16 = [](int v) { return (v + 15) & ~15; };
+    PipeLayout L;
+    const int vbytes = r16(8 * (kStreamNnz + 2));
+    const int lbytes = r16(2 * (kStreamNnz + 16));
+    const int cbytes = r16(4 * (a.max_nu + 8));
+    const int pbytes = r16(4 * (a.max_nr + 1 + 8));
+    L.off_lid = vbytes;
+    L.off_ucol = vbytes + lbytes;
+    L.off_ptr = vbytes + lbytes + cbytes;
+    L.stage_bytes = vbytes + lbytes + cbytes + pbytes;
+    L.off_xl = kStages * L.stage_bytes;
+    L.xl_doubles = std::max(a.max_nu, 2);
+    const int smem = L.off_xl + 2 * 8 * L.xl_doubles;
+    static int attr_bytes[2] = {48 * 1024, 48 * 1024};
+    if (smem > attr_bytes[MODE]) {
+      cudaError_t e = cudaFuncSetAttribute(csr_ws_kernel<MODE>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
-      attr[MODE] = true;
+      attr_bytes[MODE] = smem;
     }
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_pipe_kernel<MODE>, kStreamThreads, smem);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const int grid = std::max(1, std::min(a.nblocks, nsm * std::max(per_sm, 1)));
-    csr_pipe_kernel<MODE><<<grid, kStreamThreads, smem, st>>>(a.nblocks, a.blkinfo, a.blkucol, a.indptr,
-                                                           a.data, a.lidx, a.ucol, x, y, alpha, beta, b);
+    const int grid = std::max(1, std::min(a.nblocks, nsm));
+    csr_ws_kernel<MODE><<<grid, kPipeThreads, smem, st>>>(a.nblocks, a.blkinfo, a.blkucol, a.indptr,
+                                                          a.data, a.lidx, a.ucol, x, y, alpha, beta,
+                                                          b, L);
   }
   if (a.nlong > 0)
     csr_longrow_kernel<MODE><<<std::min((a.nlong + 127) / 128, 148), 128, 0, st>>>(
