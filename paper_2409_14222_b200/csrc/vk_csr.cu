@@ -123,7 +123,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int count) {
 //                   the stage.
 // TMA, gathers and the serial row sums of different blocks overlap, which a
 // bulk-synchronous CTA cannot do (the row sums are a dependency chain).
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 constexpr int kProdWarps = 8;
 constexpr int kConsWarps = 3;
 constexpr int kPipeThreads = 32 * (1 + kProdWarps + kConsWarps);   // 384
@@ -133,7 +133,7 @@ struct PipeLayout {
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(kPipeThreads, 1) csr_ws_kernel(
+__global__ void __launch_bounds__(kPipeThreads) csr_ws_kernel(
     int nblk, const int4* __restrict__ info, const int2* __restrict__ uinfo,
     const int* __restrict__ ptr, const double* __restrict__ val, const uint16_t* __restrict__ lidx,
     const int* __restrict__ ucol, const double* __restrict__ x, double* __restrict__ y,
@@ -188,26 +188,60 @@ __global__ void __launch_bounds__(kPipeThreads, 1) csr_ws_kernel(
     }
   } else if (warp <= kProdWarps) {
     // ------------------------------------------------------ product warps
+    // One chunk of software pipelining: the x gathers of chunk c+1 are in
+    // flight (registers) while chunk c's products are formed.
     const int t = threadIdx.x - 32;
     constexpr int NT = 32 * kProdWarps;
+    constexpr int PER = (kStreamNnz + NT - 1) / NT;    // nonzeros per thread
+    constexpr int UPT = 8;                              // unique columns per thread
+    double* xlbase = reinterpret_cast<double*>(smem + L.off_xl);
+    double xv[UPT];
+    auto gather = [&](int cc, int bk) {
+      const int s = cc % kStages;
+      mbar_wait(&full_bar[s], (cc / kStages) & 1);
+      const int4 in = __ldg(info + bk);
+      const int2 uu = __ldg(uinfo + bk);
+      const bool live = in.w > 0 && in.w <= kStreamNnz;
+      const int* sucol = reinterpret_cast<const int*>(smem + s * L.stage_bytes + L.off_ucol) +
+                         ((int64_t(uu.x) * 4) & 15) / 4;
+#pragma unroll
+      for (int j = 0; j < UPT; ++j) {
+        const int u = t + NT * j;
+        xv[j] = (live && u < uu.y) ? __ldg(x + sucol[u]) : 0.0;
+      }
+    };
     int c = 0;
+    if (blockIdx.x < nblk) gather(0, blockIdx.x);
     for (int blk = blockIdx.x; blk < nblk; blk += G, ++c) {
       const int s = c % kStages;
-      mbar_wait(&full_bar[s], (c / kStages) & 1);
       const int4 in = __ldg(info + blk);
       const int2 uu = __ldg(uinfo + blk);
       const bool live = in.w > 0 && in.w <= kStreamNnz;
-      unsigned char* st = smem + s * L.stage_bytes;
-      double* xl = reinterpret_cast<double*>(smem + L.off_xl) + (c & 1) * L.xl_doubles;
-      if (live) {
-        const int* sucol = reinterpret_cast<const int*>(st + L.off_ucol) + ((int64_t(uu.x) * 4) & 15) / 4;
-        for (int u = t; u < uu.y; u += NT) xl[u] = __ldg(x + sucol[u]);
+      double* xl = xlbase + (c & 1) * L.xl_doubles;
+#pragma unroll
+      for (int j = 0; j < UPT; ++j) {
+        const int u = t + NT * j;
+        if (live && u < uu.y) xl[u] = xv[j];
       }
       named_bar_sync(1, NT);   // every chunk: also orders xl[c&1] reuse two chunks later
+      if (blk + G < nblk) gather(c + 1, blk + G);
       if (live) {
+        unsigned char* st = smem + s * L.stage_bytes;
         double* sv = reinterpret_cast<double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
         const uint16_t* sl = reinterpret_cast<const uint16_t*>(st + L.off_lid) + ((int64_t(in.z) * 2) & 15) / 2;
-        for (int k = t; k < in.w; k += NT) sv[k] = __dmul_rn(sv[k], xl[sl[k]]);
+        int li[PER];
+        double vv[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          const int k = t + NT * q;
+          li[q] = (k < in.w) ? sl[k] : 0;
+          vv[q] = (k < in.w) ? sv[k] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          const int k = t + NT * q;
+          if (k < in.w) sv[k] = __dmul_rn(vv[q], xl[li[q]]);
+        }
       }
       mbar_arrive(&prod_bar[s]);
     }
@@ -225,12 +259,21 @@ __global__ void __launch_bounds__(kPipeThreads, 1) csr_ws_kernel(
         const double* pr = reinterpret_cast<const double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
         const int* sp = reinterpret_cast<const int*>(st + L.off_ptr) + ((int64_t(in.x) * 4) & 15) / 4;
         for (int i = t; i < in.y; i += NT) {
+          const int row = in.x + i;
+          // epilogue operand first: its load overlaps the serial sum
+          const double pre = (MODE == 1) ? __ldg(b + row) : (beta != 0.0 ? y[row] : 0.0);
           double sum = 0.0;
           if (in.w > 0) {
             const int a = sp[i] - in.z, e = sp[i + 1] - in.z;
             for (int k = a; k < e; ++k) sum = __dadd_rn(sum, pr[k]);
           }
-          store_row<MODE>(in.x + i, sum, y, alpha, beta, b);
+          if (MODE == 1) {
+            y[row] = __dsub_rn(pre, sum);
+          } else {
+            double out = (alpha == 1.0) ? sum : __dmul_rn(alpha, sum);
+            if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? pre : __dmul_rn(beta, pre), out);
+            y[row] = out;
+          }
         }
       }
       mbar_arrive(&empty_bar[s]);
@@ -276,9 +319,10 @@ cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alp
       if (e != cudaSuccess) return e;
       attr_bytes[MODE] = smem;
     }
-    int nsm = 148;
+    int nsm = 148, per_sm = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const int grid = std::max(1, std::min(a.nblocks, nsm));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_ws_kernel<MODE>, kPipeThreads, smem);
+    const int grid = std::max(1, std::min(a.nblocks, nsm * std::max(per_sm, 1)));
     csr_ws_kernel<MODE><<<grid, kPipeThreads, smem, st>>>(a.nblocks, a.blkinfo, a.blkucol, a.indptr,
                                                           a.data, a.lidx, a.ucol, x, y, alpha, beta,
                                                           b, L);
