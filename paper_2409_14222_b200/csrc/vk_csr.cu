@@ -110,26 +110,26 @@ __device__ __forceinline__ void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-// Warp-specialised, persistent CSR kernel (one CTA per SM):
-//   warp 0        : one elected thread streams each row block's value,
-//                   local-index, unique-column and row-pointer ranges into a
-//                   kStages-deep shared-memory ring with cp.async.bulk (TMA),
-//                   completion on a per-stage mbarrier;
-//   warps 1..8    : product warps — gather x at the block's unique columns
-//                   (L2) into a double-buffered table, then form the products
-//                   a_k * x_col(k) in place of the staged values;
-//   warps 9..11   : consumer warps — sum each row sequentially, left to right,
-//                   without FMA (scipy's order), apply the epilogue, release
-//                   the stage.
-// TMA, gathers and the serial row sums of different blocks overlap, which a
-// bulk-synchronous CTA cannot do (the row sums are a dependency chain).
+// Warp-specialised, persistent CSR kernel:
+//   warp 0      : one elected thread streams each row block's value,
+//                 local-index, unique-column and row-pointer ranges into a
+//                 kStages-deep shared-memory ring with cp.async.bulk (TMA),
+//                 completion on a per-stage mbarrier;
+//   warps 1..4  : gather warps — x at the block's unique columns (L2-resident)
+//                 into the stage's x table;
+//   warps 5..12 : row warps — one row per thread, summed sequentially left to
+//                 right as fl(sum + fl(a_k * x_col(k))) straight out of shared
+//                 memory (scipy's order, no FMA), epilogue, release the stage.
+// TMA streaming, gathers and the serial row sums of different blocks run
+// concurrently; products are never written back, which keeps shared-memory
+// traffic at ~28 B per nonzero.
 constexpr int kStages = 3;
-constexpr int kProdWarps = 8;
-constexpr int kConsWarps = 3;
-constexpr int kPipeThreads = 32 * (1 + kProdWarps + kConsWarps);   // 384
+constexpr int kGatherWarps = 4;
+constexpr int kRowWarps = 8;
+constexpr int kPipeThreads = 32 * (1 + kGatherWarps + kRowWarps);   // 416
 
 struct PipeLayout {
-  int stage_bytes, off_lid, off_ucol, off_ptr, off_xl, xl_doubles;
+  int stage_bytes, off_lid, off_ucol, off_ptr, off_xl;
 };
 
 template <int MODE>
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kPipeThreads) csr_ws_kernel(
     const int* __restrict__ ucol, const double* __restrict__ x, double* __restrict__ y,
     double alpha, double beta, const double* __restrict__ b, PipeLayout L) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full_bar[kStages], prod_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t full_bar[kStages], xl_bar[kStages], empty_bar[kStages];
   const int warp = threadIdx.x >> 5;
   const int G = gridDim.x;
   auto lo16 = [](int64_t v) { return v & ~int64_t(15); };
@@ -147,8 +147,8 @@ __global__ void __launch_bounds__(kPipeThreads) csr_ws_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&prod_bar[s], 32 * kProdWarps);
-      mbar_init(&empty_bar[s], 32 * kConsWarps);
+      mbar_init(&xl_bar[s], 32 * kGatherWarps);
+      mbar_init(&empty_bar[s], 32 * kRowWarps);
     }
     mbar_fence_init();
   }
@@ -186,78 +186,50 @@ __global__ void __launch_bounds__(kPipeThreads) csr_ws_kernel(
                  &full_bar[s], pol);
       }
     }
-  } else if (warp <= kProdWarps) {
-    // ------------------------------------------------------ product warps
-    // One chunk of software pipelining: the x gathers of chunk c+1 are in
-    // flight (registers) while chunk c's products are formed.
+  } else if (warp <= kGatherWarps) {
+    // ------------------------------------------------------ gather warps
     const int t = threadIdx.x - 32;
-    constexpr int NT = 32 * kProdWarps;
-    constexpr int PER = (kStreamNnz + NT - 1) / NT;    // nonzeros per thread
-    constexpr int UPT = 8;                              // unique columns per thread
-    double* xlbase = reinterpret_cast<double*>(smem + L.off_xl);
-    double xv[UPT];
-    auto gather = [&](int cc, int bk) {
-      const int s = cc % kStages;
-      mbar_wait(&full_bar[s], (cc / kStages) & 1);
-      const int4 in = __ldg(info + bk);
-      const int2 uu = __ldg(uinfo + bk);
-      const bool live = in.w > 0 && in.w <= kStreamNnz;
-      const int* sucol = reinterpret_cast<const int*>(smem + s * L.stage_bytes + L.off_ucol) +
-                         ((int64_t(uu.x) * 4) & 15) / 4;
-#pragma unroll
-      for (int j = 0; j < UPT; ++j) {
-        const int u = t + NT * j;
-        xv[j] = (live && u < uu.y) ? __ldg(x + sucol[u]) : 0.0;
-      }
-    };
+    constexpr int NT = 32 * kGatherWarps;
+    constexpr int UPT = (kStreamNnz + NT - 1) / NT;
     int c = 0;
-    if (blockIdx.x < nblk) gather(0, blockIdx.x);
     for (int blk = blockIdx.x; blk < nblk; blk += G, ++c) {
       const int s = c % kStages;
+      mbar_wait(&full_bar[s], (c / kStages) & 1);
       const int4 in = __ldg(info + blk);
       const int2 uu = __ldg(uinfo + blk);
-      const bool live = in.w > 0 && in.w <= kStreamNnz;
-      double* xl = xlbase + (c & 1) * L.xl_doubles;
-#pragma unroll
-      for (int j = 0; j < UPT; ++j) {
-        const int u = t + NT * j;
-        if (live && u < uu.y) xl[u] = xv[j];
-      }
-      named_bar_sync(1, NT);   // every chunk: also orders xl[c&1] reuse two chunks later
-      if (blk + G < nblk) gather(c + 1, blk + G);
-      if (live) {
+      if (in.w > 0 && in.w <= kStreamNnz) {
         unsigned char* st = smem + s * L.stage_bytes;
-        double* sv = reinterpret_cast<double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
-        const uint16_t* sl = reinterpret_cast<const uint16_t*>(st + L.off_lid) + ((int64_t(in.z) * 2) & 15) / 2;
-        int li[PER];
-        double vv[PER];
+        const int* sucol = reinterpret_cast<const int*>(st + L.off_ucol) + ((int64_t(uu.x) * 4) & 15) / 4;
+        double* xl = reinterpret_cast<double*>(st + L.off_xl);
+        double xv[UPT];
 #pragma unroll
-        for (int q = 0; q < PER; ++q) {
-          const int k = t + NT * q;
-          li[q] = (k < in.w) ? sl[k] : 0;
-          vv[q] = (k < in.w) ? sv[k] : 0.0;
+        for (int j = 0; j < UPT; ++j) {
+          const int u = t + NT * j;
+          xv[j] = (u < uu.y) ? __ldg(x + sucol[u]) : 0.0;
         }
 #pragma unroll
-        for (int q = 0; q < PER; ++q) {
-          const int k = t + NT * q;
-          if (k < in.w) sv[k] = __dmul_rn(vv[q], xl[li[q]]);
+        for (int j = 0; j < UPT; ++j) {
+          const int u = t + NT * j;
+          if (u < uu.y) xl[u] = xv[j];
         }
       }
-      mbar_arrive(&prod_bar[s]);
+      mbar_arrive(&xl_bar[s]);
     }
   } else {
-    // ------------------------------------------------------ consumer warps
-    const int t = threadIdx.x - 32 * (1 + kProdWarps);
-    constexpr int NT = 32 * kConsWarps;
+    // ------------------------------------------------------ row warps
+    const int t = threadIdx.x - 32 * (1 + kGatherWarps);
+    constexpr int NT = 32 * kRowWarps;
     int c = 0;
     for (int blk = blockIdx.x; blk < nblk; blk += G, ++c) {
       const int s = c % kStages;
-      mbar_wait(&prod_bar[s], (c / kStages) & 1);
+      mbar_wait(&xl_bar[s], (c / kStages) & 1);
       const int4 in = __ldg(info + blk);
       if (in.w <= kStreamNnz) {
         unsigned char* st = smem + s * L.stage_bytes;
-        const double* pr = reinterpret_cast<const double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
+        const double* sv = reinterpret_cast<const double*>(st) + ((int64_t(in.z) * 8) & 15) / 8;
+        const uint16_t* sl = reinterpret_cast<const uint16_t*>(st + L.off_lid) + ((int64_t(in.z) * 2) & 15) / 2;
         const int* sp = reinterpret_cast<const int*>(st + L.off_ptr) + ((int64_t(in.x) * 4) & 15) / 4;
+        const double* xl = reinterpret_cast<const double*>(st + L.off_xl);
         for (int i = t; i < in.y; i += NT) {
           const int row = in.x + i;
           // epilogue operand first: its load overlaps the serial sum
@@ -265,7 +237,8 @@ __global__ void __launch_bounds__(kPipeThreads) csr_ws_kernel(
           double sum = 0.0;
           if (in.w > 0) {
             const int a = sp[i] - in.z, e = sp[i + 1] - in.z;
-            for (int k = a; k < e; ++k) sum = __dadd_rn(sum, pr[k]);
+#pragma unroll 4
+            for (int k = a; k < e; ++k) sum = __dadd_rn(sum, __dmul_rn(sv[k], xl[sl[k]]));
           }
           if (MODE == 1) {
             y[row] = __dsub_rn(pre, sum);
@@ -305,13 +278,13 @@ cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alp
     const int lbytes = r16(2 * (kStreamNnz + 16));
     const int cbytes = r16(4 * (a.max_nu + 8));
     const int pbytes = r16(4 * (a.max_nr + 1 + 8));
+    const int xbytes = r16(8 * std::max(a.max_nu, 2));
     L.off_lid = vbytes;
     L.off_ucol = vbytes + lbytes;
     L.off_ptr = vbytes + lbytes + cbytes;
-    L.stage_bytes = vbytes + lbytes + cbytes + pbytes;
-    L.off_xl = kStages * L.stage_bytes;
-    L.xl_doubles = std::max(a.max_nu, 2);
-    const int smem = L.off_xl + 2 * 8 * L.xl_doubles;
+    L.off_xl = vbytes + lbytes + cbytes + pbytes;
+    L.stage_bytes = L.off_xl + xbytes;
+    const int smem = kStages * L.stage_bytes;
     static int attr_bytes[2] = {48 * 1024, 48 * 1024};
     if (smem > attr_bytes[MODE]) {
       cudaError_t e = cudaFuncSetAttribute(csr_ws_kernel<MODE>,
