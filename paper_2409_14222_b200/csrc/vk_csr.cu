@@ -237,8 +237,22 @@ __global__ void __launch_bounds__(kPipeThreads) csr_ws_kernel(
           double sum = 0.0;
           if (in.w > 0) {
             const int a = sp[i] - in.z, e = sp[i + 1] - in.z;
-#pragma unroll 4
-            for (int k = a; k < e; ++k) sum = __dadd_rn(sum, __dmul_rn(sv[k], xl[sl[k]]));
+            // groups of 8: all shared-memory loads and products first, then
+            // the 8 dependent adds (the last group predicated, no tail loop)
+            for (int k = a; k < e; k += 8) {
+              int l[8];
+              double v[8], p[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                l[q] = (k + q < e) ? sl[k + q] : 0;
+                v[q] = (k + q < e) ? sv[k + q] : 0.0;
+              }
+#pragma unroll
+              for (int q = 0; q < 8; ++q) p[q] = __dmul_rn(v[q], xl[l[q]]);
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                if (k + q < e) sum = __dadd_rn(sum, p[q]);
+            }
           }
           if (MODE == 1) {
             y[row] = __dsub_rn(pre, sum);
