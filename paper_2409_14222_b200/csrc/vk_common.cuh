@@ -21,14 +21,15 @@ struct Csr {
   double* data = nullptr;
   double mean_row = 0.0;
   int32_t max_row = 0;
-  // warp-block schedule: blocks of <= kWarpNnz nonzeros / kWarpRows rows
+  // CSR-stream schedule: row blocks of <= kStreamNnz nonzeros / kStreamRows rows
   int32_t nblocks = 0;
-  int4* blkinfo = nullptr;     // per block {r0, nrows, k0, nnz}
+  int32_t* rowblk = nullptr;   // [nblocks+1]
 };
 
-constexpr int kWarpNnz = 256;     // nonzeros per warp block (8 per lane)
-constexpr int kWarpRows = 31;     // rows per warp block (row pointers: one per lane)
-constexpr int kWarpsPerCta = 8;
+constexpr int kStreamThreads = 256;
+constexpr int kStreamU = 8;
+constexpr int kStreamNnz = kStreamThreads * kStreamU;   // 2048 nonzeros per block
+constexpr int kStreamRows = 512;
 
 // Patch set: CSR-like layout of patch DoF lists + explicit inverses.
 struct Patches {

@@ -4,17 +4,15 @@
 // mg.py:41-45 (TransferPair.prolong / restrict — restrict through an explicit
 // transposed CSR), mg.py:270, 294 (residual b - A x).
 //
-// Warp-block CSR kernel (HBM-bound, 0.17 flop/B): the rows are cut on the
-// host into blocks of <= 256 nonzeros / 31 rows and every warp owns one block
-// (8 independent warps per CTA, only warp-level synchronisation).  Each lane
-// issues 8 coalesced (col, val) loads and the 8 x-gathers (x is L2-resident),
-// the products go to the warp's shared-memory slice, then lane i sums row i
-// sequentially, left to right, without FMA contraction:
-// y_i = ((0 + a_i0 x_0) + a_i1 x_1) + ... — the exact operation order of
-// scipy's csr_matvec (and, through the ascending-source transpose, of
-// csc_matvec for masked.T), so SpMV / residual / transfers are bit-identical
-// to the reference.  With 64 independent warps per SM the serial row sums of
-// some warps overlap the loads of the others.
+// CSR-stream kernel (HBM-bound, 0.17 flop/B): the rows are cut on the host
+// into blocks of <= 2048 nonzeros / 512 rows.  A 256-thread CTA owns one
+// block: every thread issues 8 independent coalesced (col, val) loads plus
+// the 8 x-gathers (x is L2-resident), and stores the products in shared
+// memory; then each row is summed sequentially, left to right, without FMA
+// contraction: y_i = ((0 + a_i0 x_0) + a_i1 x_1) + ...  — the exact
+// operation order of scipy's csr_matvec (and, through the ascending-source
+// transpose, of csc_matvec for masked.T), so SpMV / residual / transfers are
+// bit-identical to the reference.
 #include <algorithm>
 #include <cstdarg>
 #include <cstring>
@@ -45,82 +43,96 @@ extern "C" int vk_device_sync(void) {
 
 namespace {
 
-using vk::kWarpNnz;
-using vk::kWarpRows;
-using vk::kWarpsPerCta;
-
-template <int MODE>
-__device__ __forceinline__ void store_row(int row, double s, double pre, double* __restrict__ y,
-                                          double alpha, double beta) {
-  if (MODE == 1) {
-    y[row] = __dsub_rn(pre, s);
-  } else {
-    double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
-    if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? pre : __dmul_rn(beta, pre), out);
-    y[row] = out;
-  }
-}
+using vk::kStreamNnz;
+using vk::kStreamRows;
+using vk::kStreamThreads;
+using vk::kStreamU;
 
 // MODE 0: y = alpha*Ax + beta*y (beta == 0: y not read);  MODE 1: y = b - A x
 template <int MODE>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) csr_warp_kernel(
-    int nblk, const int4* __restrict__ info, const int* __restrict__ ptr,
-    const int* __restrict__ col, const double* __restrict__ val, const double* __restrict__ x,
-    double* __restrict__ y, double alpha, double beta, const double* __restrict__ b) {
-  __shared__ double prod_all[kWarpsPerCta][kWarpNnz];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int blk = blockIdx.x * kWarpsPerCta + warp;
-  if (blk >= nblk) return;
-  double* prod = prod_all[warp];
-  const int4 in = __ldg(info + blk);              // r0, nrows, k0, nnz
-  const int nr = in.y, k0 = in.z, k1 = in.z + in.w;
-  // row pointer of row lane (lane == nr: the end pointer) and the epilogue
-  // operand, issued first so their latency overlaps the stream
-  const int p = (lane <= nr) ? __ldg(ptr + in.x + lane) : 0;
-  double pre = 0.0;
-  if (lane < nr) pre = (MODE == 1) ? __ldg(b + in.x + lane) : (beta != 0.0 ? y[in.x + lane] : 0.0);
-  double carry = 0.0;                              // single long row: lane 0's running sum
-  for (int kc = k0; kc < k1; kc += kWarpNnz) {
-    const int kend = min(k1, kc + kWarpNnz);
-    int c[8];
-    double v[8];
+__global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
+    const int* __restrict__ rowblk, const int* __restrict__ ptr, const int* __restrict__ col,
+    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+    double alpha, double beta, const double* __restrict__ b) {
+  __shared__ double prod[kStreamNnz];
+  __shared__ int sptr[kStreamRows + 1];
+  __shared__ double carry;
+  const int t = threadIdx.x;
+  const int r0 = rowblk[blockIdx.x], r1 = rowblk[blockIdx.x + 1];
+  const int nr = r1 - r0;
+  for (int i = t; i <= nr; i += kStreamThreads) sptr[i] = ptr[r0 + i];
+  // epilogue operands of this thread's rows, loaded up front so their
+  // latency overlaps the stream (rows t and t + 256 of the block)
+  double pre0 = 0.0, pre1 = 0.0;
+  if (MODE == 1 || beta != 0.0) {
+    const double* src = (MODE == 1) ? b : y;
+    if (t < nr) pre0 = src[r0 + t];
+    if (t + kStreamThreads < nr) pre1 = src[r0 + t + kStreamThreads];
+  }
+  __syncthreads();
+  const int k0 = sptr[0], k1 = sptr[nr];
+  const bool single = (nr == 1);
+  if (t == 0) carry = 0.0;
+  for (int kc = k0; kc < k1 || (kc == k0 && k0 == k1); kc += kStreamNnz) {
+    const int kend = min(k1, kc + kStreamNnz);
+    int c[kStreamU];
+    double v[kStreamU];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int k = kc + lane + 32 * u;
+    for (int u = 0; u < kStreamU; ++u) {
+      const int k = kc + t + u * kStreamThreads;
       c[u] = (k < kend) ? __ldcs(col + k) : 0;
       v[u] = (k < kend) ? __ldcs(val + k) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int k = kc + lane + 32 * u;
+    for (int u = 0; u < kStreamU; ++u) {
+      const int k = kc + t + u * kStreamThreads;
       if (k < kend) prod[k - kc] = __dmul_rn(v[u], __ldg(x + c[u]));
     }
-    __syncwarp();
-    if (nr == 1) {
-      if (lane == 0)
-        for (int k = 0; k < kend - kc; ++k) carry = __dadd_rn(carry, prod[k]);
+    __syncthreads();
+    if (single) {
+      // a row longer than one chunk: thread 0 carries the sequential sum
+      if (t == 0) {
+        double s = carry;
+        for (int k = kc; k < kend; ++k) s = __dadd_rn(s, prod[k - kc]);
+        carry = s;
+      }
     } else {
-      const int e = __shfl_down_sync(0xffffffffu, p, 1);
-      if (lane < nr) {
+      for (int i = t; i < nr; i += kStreamThreads) {
+        const int a = sptr[i] - kc, e = sptr[i + 1] - kc;
         double s = 0.0;
-        for (int k = p - kc; k < e - kc; ++k) s = __dadd_rn(s, prod[k]);
-        store_row<MODE>(in.x + lane, s, pre, y, alpha, beta);
+        for (int k = a; k < e; ++k) s = __dadd_rn(s, prod[k]);
+        const int row = r0 + i;
+        const double pre = (i < kStreamThreads) ? pre0 : (i < 2 * kStreamThreads ? pre1 : (MODE == 1 ? b[row] : y[row]));
+        if (MODE == 1) {
+          y[row] = __dsub_rn(pre, s);
+        } else {
+          double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
+          if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? pre : __dmul_rn(beta, pre), out);
+          y[row] = out;
+        }
       }
     }
-    __syncwarp();
+    __syncthreads();
+    if (k0 == k1) break;
   }
-  if (k0 == k1 && lane < nr) store_row<MODE>(in.x + lane, 0.0, pre, y, alpha, beta);
-  if (nr == 1 && k1 > k0 && lane == 0) store_row<MODE>(in.x, carry, pre, y, alpha, beta);
+  if (single && t == 0) {
+    const double s = carry;
+    if (MODE == 1) {
+      y[r0] = __dsub_rn(b[r0], s);
+    } else {
+      double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
+      if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[r0] : __dmul_rn(beta, y[r0]), out);
+      y[r0] = out;
+    }
+  }
 }
 
 template <int MODE>
 cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alpha, double beta,
                         const double* b, cudaStream_t st) {
   if (a.nblocks == 0) return cudaSuccess;
-  const int grid = (a.nblocks + kWarpsPerCta - 1) / kWarpsPerCta;
-  csr_warp_kernel<MODE><<<grid, 32 * kWarpsPerCta, 0, st>>>(a.nblocks, a.blkinfo, a.indptr, a.indices,
-                                                            a.data, x, y, alpha, beta, b);
+  csr_stream_kernel<MODE><<<a.nblocks, kStreamThreads, 0, st>>>(a.rowblk, a.indptr, a.indices,
+                                                               a.data, x, y, alpha, beta, b);
   return cudaGetLastError();
 }
 
@@ -136,23 +148,24 @@ __global__ void csr_to_dense_kernel(int nrows, int ncols, const int* __restrict_
   }
 }
 
-// greedy warp blocks: <= kWarpNnz nonzeros and <= kWarpRows rows; a row
-// longer than kWarpNnz gets a block of its own (summed chunk by chunk)
-std::vector<int4> make_row_blocks(const std::vector<int32_t>& p) {
+// greedy row blocks: <= kStreamNnz nonzeros and <= kStreamRows rows; a row
+// longer than kStreamNnz gets a block of its own
+std::vector<int32_t> make_row_blocks(const std::vector<int32_t>& p) {
   const int32_t n = static_cast<int32_t>(p.size()) - 1;
-  std::vector<int4> rb;
+  std::vector<int32_t> rb;
+  rb.push_back(0);
   int32_t r = 0;
   while (r < n) {
-    const int32_t start = r;
+    int32_t start = r;
     int64_t nnz = 0;
-    while (r < n && r - start < kWarpRows) {
+    while (r < n && r - start < kStreamRows) {
       const int64_t len = p[r + 1] - p[r];
-      if (r > start && nnz + len > kWarpNnz) break;
+      if (r > start && nnz + len > kStreamNnz) break;
       nnz += len;
       ++r;
-      if (nnz > kWarpNnz) break;  // single long row
+      if (nnz > kStreamNnz) break;  // single long row
     }
-    rb.push_back(make_int4(start, r - start, p[start], static_cast<int32_t>(nnz)));
+    rb.push_back(r);
   }
   return rb;
 }
@@ -175,15 +188,14 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
   a->nrows = nrows;
   a->ncols = ncols;
   a->nnz = nnz;
-  a->nblocks = static_cast<int32_t>(rb.size());
+  a->nblocks = static_cast<int32_t>(rb.size()) - 1;
   e = cudaMalloc(&a->indptr, sizeof(int32_t) * (nrows + 1));
   if (e == cudaSuccess) e = cudaMalloc(&a->indices, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
   if (e == cudaSuccess) e = cudaMalloc(&a->data, sizeof(double) * std::max<int64_t>(nnz, 1));
-  if (e == cudaSuccess) e = cudaMalloc(&a->blkinfo, sizeof(int4) * std::max<size_t>(rb.size(), 1));
+  if (e == cudaSuccess) e = cudaMalloc(&a->rowblk, sizeof(int32_t) * rb.size());
   if (e == cudaSuccess)
     e = cudaMemcpy(a->indptr, hp.data(), sizeof(int32_t) * (nrows + 1), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && !rb.empty())
-    e = cudaMemcpy(a->blkinfo, rb.data(), sizeof(int4) * rb.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(a->rowblk, rb.data(), sizeof(int32_t) * rb.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && nnz)
     e = cudaMemcpy(a->indices, indices, sizeof(int32_t) * nnz, cudaMemcpyDefault);
   if (e == cudaSuccess && nnz) e = cudaMemcpy(a->data, data, sizeof(double) * nnz, cudaMemcpyDefault);
@@ -192,7 +204,7 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
     cudaFree(a->indptr);
     cudaFree(a->indices);
     cudaFree(a->data);
-    cudaFree(a->blkinfo);
+    cudaFree(a->rowblk);
     delete a;
     return VK_ERR_CUDA;
   }
@@ -244,7 +256,7 @@ extern "C" int vk_csr_destroy(vk_csr_t a) {
   cudaFree(a->indptr);
   cudaFree(a->indices);
   cudaFree(a->data);
-  cudaFree(a->blkinfo);
+  cudaFree(a->rowblk);
   delete a;
   return VK_OK;
 }
