@@ -61,14 +61,6 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
   const int r0 = rowblk[blockIdx.x], r1 = rowblk[blockIdx.x + 1];
   const int nr = r1 - r0;
   for (int i = t; i <= nr; i += kStreamThreads) sptr[i] = ptr[r0 + i];
-  // epilogue operands of this thread's rows, loaded up front so their
-  // latency overlaps the stream (rows t and t + 256 of the block)
-  double pre0 = 0.0, pre1 = 0.0;
-  if (MODE == 1 || beta != 0.0) {
-    const double* src = (MODE == 1) ? b : y;
-    if (t < nr) pre0 = src[r0 + t];
-    if (t + kStreamThreads < nr) pre1 = src[r0 + t + kStreamThreads];
-  }
   __syncthreads();
   const int k0 = sptr[0], k1 = sptr[nr];
   const bool single = (nr == 1);
@@ -102,12 +94,11 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
         double s = 0.0;
         for (int k = a; k < e; ++k) s = __dadd_rn(s, prod[k]);
         const int row = r0 + i;
-        const double pre = (i < kStreamThreads) ? pre0 : (i < 2 * kStreamThreads ? pre1 : (MODE == 1 ? b[row] : y[row]));
         if (MODE == 1) {
-          y[row] = __dsub_rn(pre, s);
+          y[row] = __dsub_rn(b[row], s);
         } else {
           double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
-          if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? pre : __dmul_rn(beta, pre), out);
+          if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[row] : __dmul_rn(beta, y[row]), out);
           y[row] = out;
         }
       }
