@@ -170,6 +170,7 @@ def run_ours(args):
     from paper_2409_14222_b200 import _lib as L
     from paper_2409_14222_b200.pack import read_pack
     from paper_2409_14222_b200.solver import FgmresSolver, mg_rhs
+    from paper_2409_14222_b200.replicas import job_throughput, max_over_ranks
 
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
@@ -238,38 +239,32 @@ def run_ours(args):
     ms_total = start.elapsed_time(stop)
     ms_solve = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
     ms_gather = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
-    tmax = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    ms_total = float(tmax.item())
+    value, ms_total = job_throughput(J * args.steps, ms_total, dev)
     ms_step = ms_total / args.steps
-    value = world * J * args.steps / (ms_total * 1e-3)
 
-    # ---- e2e through the public API: pinned host residual in, host out
-    r_host = torch.from_numpy(np.random.default_rng(1).uniform(-1.0, 1.0, N)).pin_memory()
-    out_host = torch.empty(N, dtype=torch.float64).pin_memory()
-    rd = torch.empty(N, dtype=torch.float64, device=dev)
-    od = torch.empty(N, dtype=torch.float64, device=dev)
-
-    def e2e_step():
-        rd.copy_(r_host, non_blocking=True)
-        V.apply_additive(ps, rd, od, scale=0.5, mode=L.VK_APPLY_XSET)
-        out_host.copy_(od, non_blocking=True)
-
-    for _ in range(3):
-        e2e_step()
+    # ---- e2e through the public API: every step copies its residual from
+    # pinned host memory and its result back (SweepStream overlaps the copies
+    # of neighbouring steps with the sweep on three streams)
+    nbuf = 4
+    r_host = [torch.from_numpy(np.random.default_rng(10 + i).uniform(-1.0, 1.0, N)).pin_memory()
+              for i in range(nbuf)]
+    o_host = [torch.empty(N, dtype=torch.float64).pin_memory() for _ in range(nbuf)]
+    sweeps = V.SweepStream(ps, scale=0.5, mode=L.VK_APPLY_XSET)
+    ins = [r_host[k % nbuf] for k in range(args.steps)]
+    outs = [o_host[k % nbuf] for k in range(args.steps)]
+    sweeps.run(ins[:3], outs[:3])
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
+    sweeps.run(ins, outs)
     e1.record(stream)
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1) / args.steps
-    te = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * J / (float(te.item()) * 1e-3)
+    # the last result must equal a plain device sweep of the same residual
+    chk = torch.empty(N, dtype=torch.float64, device=dev)
+    V.apply_additive(ps, ins[-1].to(dev), chk, scale=0.5, mode=L.VK_APPLY_XSET)
+    assert torch.equal(chk.cpu(), outs[-1]), "pipelined e2e sweep differs from the device sweep"
+    e2e_value, _ = job_throughput(J, ms_e2e, dev)
 
     # ---- MG-FGMRES(30) time-to-solution, fine grid b
     solver = FgmresSolver(hier)

@@ -9,11 +9,12 @@ numerics run in ``libvanka_b200.so`` (hand-written CUDA behind a C ABI,
 """
 
 from .pack import ProblemPack, read_pack
-from .sparsela import (DenseFactorization, DeviceCSR, KrylovReport, NullspaceProjector,
+from .sparsela import (DenseFactorization, DeviceCSR, FgmresWorkspace, KrylovReport,
+                       NullspaceProjector,
                        SingularMatrixError, device_csr, estimate_lambda_max,
                        extract_submatrix, fgmres, lu_factor, lu_solve, nullspace_projector,
                        spmv, triple_product)
-from .vanka import (EntityRef, Patch, PatchSet, apply_additive, build_patches,
+from .vanka import (EntityRef, Patch, PatchSet, SweepStream, apply_additive, build_patches,
                     build_patches_hdiv_extended, build_patches_taylor_hood, factor_patches)
 from .mg import (ChebyshevParams, FixedDamping, Level, MgHierarchy, TransferPair,
                  chebyshev_iteration, chebyshev_relax, coarse_solve, hierarchy_from_pack,

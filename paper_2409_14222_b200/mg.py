@@ -312,6 +312,8 @@ def make_preconditioner(hier: MgHierarchy, nu=None, mode=None):
             return hier.vcycle_device(r, nu, mode)
         return v_cycle(hier, r, nu, mode)
     prec._device = True
+    # eager (kernel-by-kernel) form, recorded into FGMRES step graphs
+    prec._eager = lambda r: hier.vcycle_device(r, nu, mode, graph=False)
     return prec
 
 

@@ -12,7 +12,7 @@ from __future__ import annotations
 import numpy as np
 
 from .mg import MgHierarchy, make_preconditioner, pressure_kernel
-from .sparsela import fgmres, nullspace_projector, to_device
+from .sparsela import FgmresWorkspace, fgmres, nullspace_projector, to_device
 
 
 def mg_rhs(pack) -> np.ndarray:
@@ -38,6 +38,7 @@ class FgmresSolver:
         self.prec = make_preconditioner(hier)
         self.nsp = nullspace_projector([pressure_kernel(hier.fine.mixed)])
         self.A = hier.fine.A
+        self.workspace = FgmresWorkspace(hier.fine.n, restart)
 
     def solve(self, b):
         """Returns (x, iterations, converged, history) with x on the device
@@ -51,7 +52,8 @@ class FgmresSolver:
         conv = False
         for _ in range(self.max_cycles):
             x, rep = fgmres(self.A, bd, preconditioner=self.prec, rtol=self.rtol,
-                            max_it=self.restart, nullspace=self.nsp, x0=x, target_norm=base)
+                            max_it=self.restart, nullspace=self.nsp, x0=x, target_norm=base,
+                            workspace=self.workspace)
             if base is None:
                 pb = self.nsp(bd.clone())
                 base = float(torch.linalg.vector_norm(pb).item()) if rep.iterations else None

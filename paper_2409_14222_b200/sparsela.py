@@ -293,6 +293,7 @@ def _device_operator(a):
         def host_op(v, f=a):
             out = f(v.cpu().numpy())
             return torch.as_tensor(np.asarray(out, dtype=np.float64), device="cuda")
+        host_op._host = True
         return host_op
     d = device_csr(a)
 
@@ -304,13 +305,63 @@ def _device_operator(a):
     return op
 
 
+class FgmresWorkspace:
+    """Persistent Krylov buffers + one captured CUDA graph per Arnoldi step.
+
+    With a workspace, step j of :func:`fgmres` — preconditioner (V-cycle
+    kernels recorded eagerly into the graph), SpMV, nullspace projection,
+    the j+1 MGS dot/axpy pairs, the norm and the normalisation — is captured
+    once and replayed as a single graph launch; the host still performs the
+    Givens update in the reference's scalar arithmetic after one D2H read."""
+
+    def __init__(self, n: int, max_it: int):
+        torch = _torch()
+        self.n, self.max_it = n, max_it
+        self.vmat = torch.zeros((max_it + 1, n), dtype=torch.float64, device="cuda")
+        self.zmat = torch.zeros((max_it, n), dtype=torch.float64, device="cuda")
+        self.w = torch.empty(n, dtype=torch.float64, device="cuda")
+        self.scal = torch.zeros(max_it + 3, dtype=torch.float64, device="cuda")
+        self.graphs = {}
+        self._key = None
+
+    def fits(self, n, max_it):
+        return n == self.n and max_it == self.max_it
+
+    @staticmethod
+    def capturable(op, prec, proj):
+        return (prec is None or hasattr(prec, "_eager")) and not hasattr(op, "_host") and \
+            getattr(proj, "_device", True)
+
+    def replay(self, j, step, prec):
+        torch = _torch()
+        key = (id(prec),)
+        if key != self._key:             # a different preconditioner: recapture
+            self.graphs.clear()
+            self._key = key
+        g = self.graphs.get(j)
+        if g is None:
+            eager = prec._eager if prec is not None else None
+            step(j, eager)               # warm-up run (also this step's result)
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):   # records only; step j already ran
+                    step(j, eager)
+            torch.cuda.current_stream().wait_stream(s)
+            self.graphs[j] = g
+            return
+        g.replay()
+
+
 def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
-           nullspace=None, x0=None, target_norm=None):
+           nullspace=None, x0=None, target_norm=None, workspace: FgmresWorkspace | None = None):
     """Unrestarted flexible GMRES (reference ``sparsela.fgmres``,
     ``sparsela.py:117-191``).  Krylov/direction vectors, SpMVs, dot products,
     MGS updates and the final combination run on the device; only the
     Hessenberg column (j+2 scalars) crosses to the host once per iteration for
-    the Givens update, in exactly the reference's scalar arithmetic."""
+    the Givens update, in exactly the reference's scalar arithmetic.  With a
+    :class:`FgmresWorkspace` each Arnoldi step is one CUDA-graph replay."""
     torch = _torch()
     op = _device_operator(a)
     prec = _device_operator(preconditioner) if preconditioner is not None else None
@@ -320,6 +371,7 @@ def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
         def proj(v):
             v.copy_(torch.as_tensor(proj_host(v.cpu().numpy()), device="cuda"))
             return v
+        proj._device = False
     elif nullspace is not None:
         proj = nullspace.apply_
     else:
@@ -346,9 +398,15 @@ def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
     if beta <= rtol * base:
         return to_host(x, host), KrylovReport(0, history[0], True, np.array(history))
 
-    vmat = torch.zeros((max_it + 1, n), dtype=torch.float64, device="cuda")
-    zmat = torch.zeros((max_it, n), dtype=torch.float64, device="cuda")
-    w = torch.empty(n, dtype=torch.float64, device="cuda")
+    ws = workspace if (workspace is not None and workspace.fits(n, max_it)) else None
+    if ws is not None:
+        vmat, zmat, w = ws.vmat, ws.zmat, ws.w
+        ws.scal[max_it + 2:max_it + 3].copy_(scal[max_it + 2:max_it + 3])
+        scal = ws.scal
+    else:
+        vmat = torch.zeros((max_it + 1, n), dtype=torch.float64, device="cuda")
+        zmat = torch.zeros((max_it, n), dtype=torch.float64, device="cuda")
+        w = torch.empty(n, dtype=torch.float64, device="cuda")
     hess = np.zeros((max_it + 1, max_it))
     cs = np.zeros(max_it)
     sn = np.zeros(max_it)
@@ -356,24 +414,31 @@ def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
     g[0] = beta
     L.call("vk_div_dev", n, L.ptr(r), L.ptr(scal[max_it + 2:]), L.ptr(vmat[0]), st)
 
-    converged = False
-    breakdown = False
-    j = 0
-    for j in range(max_it):
+    def arnoldi_step(j, eager_prec):
+        s_ = _stream()
         if prec is not None:
-            z = prec(vmat[j])
+            z = eager_prec(vmat[j])
             zmat[j].copy_(z)
         else:
             zmat[j].copy_(vmat[j])
         wz = op(zmat[j])
         w.copy_(wz)
         proj(w)
-        L.call("vk_nrm2", n, L.ptr(w), L.ptr(scal[max_it + 1:]), st)      # wnorm0
-        for i in range(j + 1):
-            L.call("vk_dot", n, L.ptr(vmat[i]), L.ptr(w), L.ptr(scal[i:]), st)
-            L.call("vk_axpy_dev", n, L.ptr(scal[i:]), L.ptr(vmat[i]), L.ptr(w), st)
-        L.call("vk_nrm2", n, L.ptr(w), L.ptr(scal[j + 1:]), st)
-        L.call("vk_div_dev", n, L.ptr(w), L.ptr(scal[j + 1:]), L.ptr(vmat[j + 1]), st)
+        L.call("vk_nrm2", n, L.ptr(w), L.ptr(scal[max_it + 1:]), s_)      # wnorm0
+        for i in range(j + 1):                                            # MGS (sparsela.py:160-163)
+            L.call("vk_dot", n, L.ptr(vmat[i]), L.ptr(w), L.ptr(scal[i:]), s_)
+            L.call("vk_axpy_dev", n, L.ptr(scal[i:]), L.ptr(vmat[i]), L.ptr(w), s_)
+        L.call("vk_nrm2", n, L.ptr(w), L.ptr(scal[j + 1:]), s_)
+        L.call("vk_div_dev", n, L.ptr(w), L.ptr(scal[j + 1:]), L.ptr(vmat[j + 1]), s_)
+
+    converged = False
+    breakdown = False
+    j = 0
+    for j in range(max_it):
+        if ws is not None and ws.capturable(op, prec, proj):
+            ws.replay(j, arnoldi_step, prec)       # one CUDA graph per Arnoldi step
+        else:
+            arnoldi_step(j, prec)
         hs = scal.cpu().numpy()                                           # 1 sync
         hess[:j + 2, j] = hs[:j + 2]
         wnorm0 = hs[max_it + 1]

@@ -355,6 +355,68 @@ def apply_additive(patchset: PatchSet, residual, out=None, *, scale: float = 1.0
     return to_host(out, host)
 
 
+class SweepStream:
+    """Pipelined host-to-host additive sweeps (the batched form of
+    :func:`apply_additive` for many right-hand sides held in host memory).
+
+    Three CUDA streams: the host->device copy of residual k+1 and the
+    device->host copy of result k-1 overlap the sweep of residual k; device
+    buffers rotate through ``depth`` slots guarded by events.  Every residual
+    still crosses PCIe in and every result out."""
+
+    def __init__(self, patchset: PatchSet, *, scale: float = 1.0, mode: int = L.VK_APPLY_OUT,
+                 depth: int = 3):
+        import torch
+        if not patchset.factored:
+            raise ValueError("patches must be factored")
+        self.ps = patchset
+        self.scale = scale
+        self.mode = mode
+        self.depth = depth
+        n = patchset.size
+        self.r_dev = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(depth)]
+        self.o_dev = [torch.zeros(n, dtype=torch.float64, device="cuda") for _ in range(depth)]
+        self.s_in, self.s_comp, self.s_out = (torch.cuda.Stream() for _ in range(3))
+        self.ev_in = [torch.cuda.Event() for _ in range(depth)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(depth)]
+        self.ev_out = [torch.cuda.Event() for _ in range(depth)]
+        self._used = [False] * depth
+
+    def run(self, residuals, outputs):
+        """residuals / outputs: sequences of (preferably pinned) host float64
+        tensors of length ``size``; results are in ``outputs`` once
+        :meth:`wait` (or a device synchronize) returns."""
+        import torch
+        h = self.ps.handle
+        start = torch.cuda.current_stream()
+        for s in (self.s_in, self.s_comp, self.s_out):
+            s.wait_stream(start)
+        for k, (rh, oh) in enumerate(zip(residuals, outputs)):
+            q = k % self.depth
+            with torch.cuda.stream(self.s_in):
+                if self._used[q]:
+                    self.s_in.wait_event(self.ev_comp[q])      # slot's residual consumed
+                self.r_dev[q].copy_(rh, non_blocking=True)
+                self.ev_in[q].record(self.s_in)
+            with torch.cuda.stream(self.s_comp):
+                self.s_comp.wait_event(self.ev_in[q])
+                if self._used[q]:
+                    self.s_comp.wait_event(self.ev_out[q])     # slot's result drained
+                L.call("vk_patches_apply", h, L.ptr(self.r_dev[q]), L.ptr(self.o_dev[q]),
+                       self.scale, self.mode, self.s_comp.cuda_stream)
+                self.ev_comp[q].record(self.s_comp)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(self.ev_comp[q])
+                oh.copy_(self.o_dev[q], non_blocking=True)
+                self.ev_out[q].record(self.s_out)
+            self._used[q] = True
+        start.wait_stream(self.s_out)
+        return outputs
+
+    def wait(self):
+        self.s_out.synchronize()
+
+
 def patch_inverses(patchset: PatchSet, first: int = 0, count: int | None = None) -> list:
     """Host copies of the explicit patch inverses (row-major), for tests."""
     n = patchset.num_patches

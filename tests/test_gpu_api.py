@@ -463,6 +463,28 @@ def test_single_level_is_direct_solve(V):
     assert np.linalg.norm(pack.fine.system.matrix @ x - b) < 1e-9 * np.linalg.norm(b)
 
 
+def test_fgmres_step_graphs_match_eager(V):
+    # one CUDA graph per Arnoldi step (FgmresWorkspace) == kernel-by-kernel
+    pack, _ = load_case("s_bdm3")
+    hier = V.hierarchy_from_pack(pack)
+    from paper_2409_14222_b200.solver import mg_rhs
+    b = mg_rhs(pack)
+    nsp = V.nullspace_projector([V.pressure_kernel(pack.fine.mixed)])
+    prec = V.make_preconditioner(hier)
+    A = pack.fine.system.matrix
+    x1, r1 = V.fgmres(A, b, preconditioner=prec, rtol=1e-8, max_it=30, nullspace=nsp)
+    ws = V.FgmresWorkspace(len(b), 30)
+    x2, r2 = V.fgmres(A, b, preconditioner=prec, rtol=1e-8, max_it=30, nullspace=nsp,
+                      workspace=ws)
+    x3, r3 = V.fgmres(A, b, preconditioner=prec, rtol=1e-8, max_it=30, nullspace=nsp,
+                      workspace=ws)                     # replays the captured graphs
+    assert len(ws.graphs) == r2.iterations
+    for r in (r2, r3):
+        assert r.iterations == r1.iterations
+        assert np.array_equal(r.history, r1.history)
+    assert np.array_equal(x1, x2) and np.array_equal(x1, x3)
+
+
 def test_preconditioned_solver_converges(V):
     pack, _ = load_case("s_thquad2")
     hier = V.hierarchy_from_pack(pack)
