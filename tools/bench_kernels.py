@@ -41,6 +41,7 @@ def main():
     ap.add_argument("names", nargs="*", default=["cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--json")
+    ap.add_argument("--tts", action="store_true", help="also V-cycle time and MG-FGMRES TTS")
     args = ap.parse_args()
     import torch
     import paper_2409_14222_b200 as V
@@ -104,10 +105,40 @@ def main():
             rec.update({"prolong_ms": t_pro, "restrict_ms": t_rst,
                         "prolong_gbps": b_p / (t_pro * 1e-3) / 1e9,
                         "restrict_gbps": b_t / (t_rst * 1e-3) / 1e9, "nnz_P": int(P.nnz)})
+        if args.tts and name != "cfg1":
+            from paper_2409_14222_b200.solver import FgmresSolver, mg_rhs
+            del ps
+            t0 = time.perf_counter()
+            hier = V.hierarchy_from_pack(pack)
+            torch.cuda.synchronize()
+            rec["mg_setup_s"] = time.perf_counter() - t0
+            b = torch.from_numpy(mg_rhs(pack)).cuda()
+            rec["vcycle_ms"] = timed(lambda: hier.vcycle_device(b), args.reps, st)
+            solver = FgmresSolver(hier)
+            solver.solve(b)
+            tts = []
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                _, its, conv, hist = solver.solve(b)
+                e1.record(st)
+                torch.cuda.synchronize()
+                tts.append(e0.elapsed_time(e1))
+            rec["tts_ms"] = statistics.median(tts)
+            rec["tts_iterations"] = its
+            ref = json.load(open(os.path.join(ROOT, "tests", "golden", f"{name}_history.json")))
+            rec["tts_reference_iterations"] = ref["iterations"]
+            rec["tts_reference_cpu_s"] = ref["solve_s"]
+            h_ref = np.asarray(ref["history"])
+            m = min(len(hist), len(h_ref))
+            rec["history_max_rel"] = float(np.max(np.abs(hist[:m] - h_ref[:m]) / h_ref[:m]))
+            del hier, solver
+            torch.cuda.empty_cache()
         out[name] = rec
         print(name, json.dumps({k: (round(v, 4) if isinstance(v, float) else v)
                                 for k, v in rec.items()}), flush=True)
-        del ps
+        if "ps" in locals():
+            del ps
     if args.json:
         json.dump(out, open(args.json, "w"), indent=1)
 
