@@ -237,6 +237,148 @@ std::vector<Bucket> make_buckets(const std::vector<int64_t>& off, int first, int
   return b;
 }
 
+// Small patches (s <= 64): one WARP per patch, several independent patches per
+// CTA (no block barriers; only __syncwarp).  Same algorithm and arithmetic
+// as factor_kernel: verbatim extraction, row-scale guard, Gauss-Jordan with
+// LAPACK-order partial pivoting and the reference pivot test, column-major
+// inverse with the column permutation undone.  Lane j keeps pivot-row
+// entries j and j+32 in registers during each elimination step.
+constexpr int kFactorWarps = 4;
+
+__host__ __device__ inline size_t warp_slice_doubles(int smax) {
+  // block + row scales, then 3 int arrays (idx, perm, iperm) packed in doubles
+  return size_t(smax) * lda_of(smax) + smax + (3 * size_t(smax) + 1) / 2;
+}
+
+__global__ void __launch_bounds__(32 * kFactorWarps) factor_warp_kernel(
+    const int* __restrict__ plist, int count, int smax, const int64_t* __restrict__ off,
+    const int* __restrict__ idx, const int* __restrict__ ptr, const int* __restrict__ col,
+    const double* __restrict__ val, const int64_t* __restrict__ opoff, double* __restrict__ inv,
+    int* __restrict__ status) {
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  double* A = smem + warp * warp_slice_doubles(smax);
+  const int gw = blockIdx.x * kFactorWarps + warp;
+  const int nw = gridDim.x * kFactorWarps;
+  for (int b = gw; b < count; b += nw) {
+    const int p = plist[b];
+    const int64_t base = off[p];
+    const int s = static_cast<int>(off[p + 1] - base);
+    const int ld = lda_of(s);
+    double* rs = A + size_t(s) * ld;
+    int* sidx = reinterpret_cast<int*>(rs + s);
+    int* perm = sidx + s;
+    int* iperm = perm + s;
+    for (int i = lane; i < s; i += 32) {
+      sidx[i] = idx[base + i];
+      perm[i] = i;
+    }
+    for (int e = lane; e < s * ld; e += 32) A[e] = 0.0;
+    __syncwarp();
+    // 1. extraction: lane per block row, binary search of each CSR column
+    for (int i = lane; i < s; i += 32) {
+      const int row = sidx[i];
+      for (int k = ptr[row]; k < ptr[row + 1]; ++k) {
+        const int c = col[k];
+        int lo = 0, hi = s - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (sidx[mid] < c) lo = mid + 1; else hi = mid;
+        }
+        if (sidx[lo] == c) A[i * ld + lo] = val[k];
+      }
+    }
+    __syncwarp();
+    // 2. row scales / all-zero-row guard
+    int bad = 0;
+    for (int i = lane; i < s; i += 32) {
+      double m = 0.0;
+      for (int j = 0; j < s; ++j) m = fmax(m, fabs(A[i * ld + j]));
+      rs[i] = m;
+      if (m == 0.0) bad = 1;
+    }
+    if (__any_sync(0xffffffffu, bad)) {
+      if (lane == 0) status[p] = VK_PATCH_ZERO_ROW;
+      __syncwarp();
+      continue;
+    }
+    __syncwarp();
+    // 3. Gauss-Jordan with partial pivoting
+    int st = VK_PATCH_OK;
+    for (int k = 0; k < s; ++k) {
+      double best = -1.0;
+      int bi = s;
+      for (int i = k + lane; i < s; i += 32) {
+        const double v = fabs(A[i * ld + k]);
+        if (v > best) {
+          best = v;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (bi != k) {
+        for (int j = lane; j < s; j += 32) {
+          const double t = A[k * ld + j];
+          A[k * ld + j] = A[bi * ld + j];
+          A[bi * ld + j] = t;
+        }
+        if (lane == 0) {
+          const int t = perm[k];
+          perm[k] = perm[bi];
+          perm[bi] = t;
+        }
+      }
+      __syncwarp();
+      const double piv = A[k * ld + k];
+      if (!(fabs(piv) >= 1e-12 * rs[perm[k]])) {   // warp-uniform
+        st = VK_PATCH_SMALL_PIVOT;
+        break;
+      }
+      const double rinv = 1.0 / piv;
+      // scaled pivot row in registers: entries lane, lane + 32
+      const int j0 = lane, j1 = lane + 32;
+      double pk0 = 0.0, pk1 = 0.0;
+      if (j0 < s) pk0 = (j0 == k) ? rinv : A[k * ld + j0] * rinv;
+      if (j1 < s) pk1 = (j1 == k) ? rinv : A[k * ld + j1] * rinv;
+      __syncwarp();
+      if (j0 < s) A[k * ld + j0] = pk0;
+      if (j1 < s) A[k * ld + j1] = pk1;
+      for (int i = 0; i < s; ++i) {
+        if (i == k) continue;
+        const double f = A[i * ld + k];
+        __syncwarp();
+        if (j0 < s) A[i * ld + j0] = (j0 == k) ? -f * rinv : fma(-f, pk0, A[i * ld + j0]);
+        if (j1 < s) A[i * ld + j1] = (j1 == k) ? -f * rinv : fma(-f, pk1, A[i * ld + j1]);
+      }
+      __syncwarp();
+    }
+    if (st != VK_PATCH_OK) {
+      if (lane == 0) status[p] = st;
+      __syncwarp();
+      continue;
+    }
+    // 4. Ainv[i][j] = X[i][iperm[j]], written column-major
+    for (int q = lane; q < s; q += 32) iperm[perm[q]] = q;
+    __syncwarp();
+    double* dst = inv + opoff[p];
+    for (int e = lane; e < s * s; e += 32) {
+      const int j = e / s, i = e - j * s;
+      dst[e] = A[i * ld + iperm[j]];
+    }
+    if (lane == 0) status[p] = VK_PATCH_OK;
+    __syncwarp();
+  }
+}
+
 int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int* d_status,
                   double* blocks, const std::vector<int64_t>* blk_off_host, int extract_only,
                   cudaStream_t st) {
@@ -252,7 +394,18 @@ int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int
   }
   const size_t smem = factor_smem_bytes(bk.smax);
   const int count = static_cast<int>(bk.ids.size());
-  if (bk.smax <= 32) {
+  if (!extract_only && bk.smax <= 64) {
+    const size_t wsm = sizeof(double) * warp_slice_doubles(bk.smax) * kFactorWarps;
+    VK_CHECK_CUDA(cudaFuncSetAttribute(factor_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(wsm)));
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_warp_kernel, 32 * kFactorWarps, wsm);
+    const int grid = std::max(1, std::min((count + kFactorWarps - 1) / kFactorWarps,
+                                          148 * std::max(per_sm, 1)));
+    factor_warp_kernel<<<grid, 32 * kFactorWarps, wsm, st>>>(d_ids, count, bk.smax, h->off, h->idx,
+                                                            a->indptr, a->indices, a->data, h->opoff,
+                                                            h->inv, d_status);
+  } else if (bk.smax <= 32) {
     VK_CHECK_CUDA(cudaFuncSetAttribute(factor_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(smem)));
     factor_kernel<128><<<std::min(count, 148 * 32), 128, smem, st>>>(
