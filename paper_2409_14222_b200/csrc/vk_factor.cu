@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(
   __shared__ int s_piv;
   __shared__ int s_status;
   constexpr int NW = NT / 32;
+  constexpr int QMAX = (kMaxPatch + 31) / 32;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
@@ -147,30 +148,40 @@ __global__ void __launch_bounds__(NT) factor_kernel(
           A[k * ld + j] = A[pr * ld + j];
           A[pr * ld + j] = t;
         }
+        __syncthreads();
       }
-      __syncthreads();
       const double piv = A[k * ld + k];
       if (!(fabs(piv) >= 1e-12 * rs[perm[k]])) {  // also catches NaN
         if (threadIdx.x == 0) s_status = VK_PATCH_SMALL_PIVOT;
         break;  // block-uniform: every thread sees the same piv
       }
       const double rinv = 1.0 / piv;
-      __syncthreads();  // everyone has read piv before row k changes
-      for (int j = threadIdx.x; j < s; j += NT)
-        A[k * ld + j] = (j == k) ? rinv : A[k * ld + j] * rinv;
-      __syncthreads();
+      // scaled pivot row in registers (columns lane + 32 q); row k itself is
+      // rewritten only after every warp has finished this step
+      double pk[QMAX];
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) {
+        const int j = lane + 32 * q;
+        pk[q] = (j < s) ? ((j == k) ? rinv : A[k * ld + j] * rinv) : 0.0;
+      }
       for (int i = warp; i < s; i += NW) {
         if (i == k) continue;
         const double f = A[i * ld + k];
         __syncwarp();
-        for (int j = lane; j < s; j += 32) {
-          if (j == k)
-            A[i * ld + k] = -f * rinv;
-          else
-            A[i * ld + j] = fma(-f, A[k * ld + j], A[i * ld + j]);
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) {
+          const int j = lane + 32 * q;
+          if (j < s) A[i * ld + j] = (j == k) ? -f * rinv : fma(-f, pk[q], A[i * ld + j]);
         }
       }
       __syncthreads();
+      if (warp == 0) {
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) {
+          const int j = lane + 32 * q;
+          if (j < s) A[k * ld + j] = pk[q];
+        }
+      }
     }
     __syncthreads();
     if (s_status != 0) {
@@ -304,8 +315,10 @@ __global__ void __launch_bounds__(32 * kFactorWarps) factor_warp_kernel(
       continue;
     }
     __syncwarp();
-    // 3. Gauss-Jordan with partial pivoting
+    // 3. Gauss-Jordan with partial pivoting; lanes own rows (lane, lane+32)
+    //    and sweep the columns, reading the scaled pivot row as broadcasts
     int st = VK_PATCH_OK;
+    const int i0 = lane, i1 = lane + 32;
     for (int k = 0; k < s; ++k) {
       double best = -1.0;
       int bi = s;
@@ -344,20 +357,23 @@ __global__ void __launch_bounds__(32 * kFactorWarps) factor_warp_kernel(
         break;
       }
       const double rinv = 1.0 / piv;
-      // scaled pivot row in registers: entries lane, lane + 32
-      const int j0 = lane, j1 = lane + 32;
-      double pk0 = 0.0, pk1 = 0.0;
-      if (j0 < s) pk0 = (j0 == k) ? rinv : A[k * ld + j0] * rinv;
-      if (j1 < s) pk1 = (j1 == k) ? rinv : A[k * ld + j1] * rinv;
+      const bool u0 = i0 < s && i0 != k, u1 = i1 < s && i1 != k;
+      const double f0 = u0 ? A[i0 * ld + k] : 0.0;
+      const double f1 = u1 ? A[i1 * ld + k] : 0.0;
+      __syncwarp();                     // column k read before row k is scaled
+      for (int j = lane; j < s; j += 32)
+        A[k * ld + j] = (j == k) ? rinv : A[k * ld + j] * rinv;
       __syncwarp();
-      if (j0 < s) A[k * ld + j0] = pk0;
-      if (j1 < s) A[k * ld + j1] = pk1;
-      for (int i = 0; i < s; ++i) {
-        if (i == k) continue;
-        const double f = A[i * ld + k];
-        __syncwarp();
-        if (j0 < s) A[i * ld + j0] = (j0 == k) ? -f * rinv : fma(-f, pk0, A[i * ld + j0]);
-        if (j1 < s) A[i * ld + j1] = (j1 == k) ? -f * rinv : fma(-f, pk1, A[i * ld + j1]);
+#pragma unroll 4
+      for (int j = 0; j < s; ++j) {
+        const double pj = A[k * ld + j];              // broadcast
+        if (j == k) {
+          if (u0) A[i0 * ld + k] = -f0 * rinv;
+          if (u1) A[i1 * ld + k] = -f1 * rinv;
+        } else {
+          if (u0) A[i0 * ld + j] = fma(-f0, pj, A[i0 * ld + j]);
+          if (u1) A[i1 * ld + j] = fma(-f1, pj, A[i1 * ld + j]);
+        }
       }
       __syncwarp();
     }
@@ -411,10 +427,16 @@ int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int
     factor_kernel<128><<<std::min(count, 148 * 32), 128, smem, st>>>(
         d_ids, count, h->off, h->idx, a->indptr, a->indices, a->data, h->opoff, h->inv, d_status,
         blocks, d_boff, extract_only);
-  } else {
+  } else if (bk.smax <= 64) {
     VK_CHECK_CUDA(cudaFuncSetAttribute(factor_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(smem)));
     factor_kernel<256><<<std::min(count, 148 * 16), 256, smem, st>>>(
+        d_ids, count, h->off, h->idx, a->indptr, a->indices, a->data, h->opoff, h->inv, d_status,
+        blocks, d_boff, extract_only);
+  } else {
+    VK_CHECK_CUDA(cudaFuncSetAttribute(factor_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(smem)));
+    factor_kernel<512><<<std::min(count, 148 * 8), 512, smem, st>>>(
         d_ids, count, h->off, h->idx, a->indptr, a->indices, a->data, h->opoff, h->inv, d_status,
         blocks, d_boff, extract_only);
   }
