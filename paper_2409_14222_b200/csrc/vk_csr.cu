@@ -254,8 +254,9 @@ extern "C" int vk_csr_destroy(vk_csr_t a) {
 
 extern "C" int vk_spmv(vk_csr_t a, const double* x, double* y, double alpha, double beta,
                        void* stream) {
-  VK_REQUIRE(a && x && y, "vk_spmv: null argument");
-  if (a->nrows == 0) return VK_OK;
+  VK_REQUIRE(a, "vk_spmv: null matrix");
+  if (a->nrows == 0) return VK_OK;  // empty output: nothing to touch
+  VK_REQUIRE((x || a->ncols == 0) && y, "vk_spmv: null argument");
   cudaError_t e = launch_spmv<0>(*a, x, y, alpha, beta, nullptr, vk_stream(stream));
   if (e != cudaSuccess) {
     vk::set_error("vk_spmv: %s", cudaGetErrorString(e));
@@ -265,9 +266,10 @@ extern "C" int vk_spmv(vk_csr_t a, const double* x, double* y, double alpha, dou
 }
 
 extern "C" int vk_residual(vk_csr_t a, const double* b, const double* x, double* r, void* stream) {
-  VK_REQUIRE(a && b && x && r, "vk_residual: null argument");
+  VK_REQUIRE(a, "vk_residual: null matrix");
   VK_REQUIRE(a->nrows == a->ncols, "vk_residual: matrix must be square");
   if (a->nrows == 0) return VK_OK;
+  VK_REQUIRE(b && x && r, "vk_residual: null argument");
   cudaError_t e = launch_spmv<1>(*a, x, r, 1.0, 0.0, b, vk_stream(stream));
   if (e != cudaSuccess) {
     vk::set_error("vk_residual: %s", cudaGetErrorString(e));
