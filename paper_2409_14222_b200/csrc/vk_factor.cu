@@ -31,7 +31,67 @@ constexpr int kMaxPatch = 164;  // s*(s|1)*8 + 20 s bytes <= 227 KB
 __host__ __device__ inline int lda_of(int s) { return s | 1; }
 
 inline size_t factor_smem_bytes(int s) {
-  return sizeof(double) * (size_t(s) * lda_of(s) + s) + sizeof(int) * 3 * size_t(s);
+  return sizeof(double) * (size_t(s) * lda_of(s) + s) + sizeof(int) * (5 * size_t(s) + 1);
+}
+
+// One warp: rowoff[i+1] holds row i's length on entry, the exclusive prefix
+// (row offsets into the flattened entry list) on exit.
+__device__ __forceinline__ void warp_scan_rows(int lane, int s, int* rowoff) {
+  int carry = 0;
+  for (int base = 0; base < s; base += 32) {
+    const int i = base + lane;
+    int v = (i < s) ? rowoff[i + 1] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += n;
+    }
+    if (i < s) rowoff[i + 1] = v + carry;
+    carry += __shfl_sync(0xffffffffu, v, 31);
+  }
+  if (lane == 0) rowoff[0] = 0;
+}
+
+// Extraction of the dense patch block A[idx, idx] from the CSR with every
+// (row, stored entry) pair as an independent work item: thread t takes
+// entries t, t + nth, ..., four in flight, finds its row by binary search in
+// the row offsets and its column by binary search in the sorted patch list,
+// and copies the stored value verbatim (absent entries stay +0.0).
+__device__ __forceinline__ void extract_entries(int tid, int nth, int s, int ld, const int* sidx,
+                                                const int* rowoff, const int* rowk0,
+                                                const int* __restrict__ col,
+                                                const double* __restrict__ val, double* A) {
+  const int E = rowoff[s];
+  for (int e0 = tid; e0 < E; e0 += 4 * nth) {
+    int rw[4], c[4];
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * nth;
+      rw[u] = -1;
+      if (e < E) {
+        int lo = 0, hi = s - 1;           // last row with rowoff[row] <= e
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (rowoff[mid] <= e) lo = mid; else hi = mid - 1;
+        }
+        const int k = rowk0[lo] + (e - rowoff[lo]);
+        rw[u] = lo;
+        c[u] = __ldg(col + k);
+        v[u] = __ldg(val + k);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (rw[u] < 0) continue;
+      int lo = 0, hi = s - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sidx[mid] < c[u]) lo = mid + 1; else hi = mid;
+      }
+      if (sidx[lo] == c[u]) A[rw[u] * ld + lo] = v[u];
+    }
+  }
 }
 
 template <int NT>
@@ -59,29 +119,25 @@ __global__ void __launch_bounds__(NT) factor_kernel(
     int* sidx = reinterpret_cast<int*>(rs + s);
     int* perm = sidx + s;
     int* iperm = perm + s;
+    int* rowoff = iperm + s;      // s + 1
+    int* rowk0 = rowoff + s + 1;  // s
 
     for (int i = threadIdx.x; i < s; i += NT) {
-      sidx[i] = idx[base + i];
+      const int r = idx[base + i];
+      sidx[i] = r;
       perm[i] = i;
+      const int a = ptr[r];
+      rowk0[i] = a;
+      rowoff[i + 1] = ptr[r + 1] - a;
     }
     for (int e = threadIdx.x; e < s * ld; e += NT) A[e] = 0.0;
     if (threadIdx.x == 0) s_status = 0;
     __syncthreads();
+    if (warp == 0) warp_scan_rows(lane, s, rowoff);
+    __syncthreads();
 
     // 1. extraction (bit-exact copy of stored entries)
-    for (int i = warp; i < s; i += NW) {
-      const int row = sidx[i];
-      const int k0 = ptr[row], k1 = ptr[row + 1];
-      for (int k = k0 + lane; k < k1; k += 32) {
-        const int c = col[k];
-        int lo = 0, hi = s - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (sidx[mid] < c) lo = mid + 1; else hi = mid;
-        }
-        if (sidx[lo] == c) A[i * ld + lo] = val[k];
-      }
-    }
+    extract_entries(threadIdx.x, NT, s, ld, sidx, rowoff, rowk0, col, val, A);
     __syncthreads();
     if (blocks_out) {
       double* dst = blocks_out + blk_off[b];
@@ -257,8 +313,8 @@ std::vector<Bucket> make_buckets(const std::vector<int64_t>& off, int first, int
 constexpr int kFactorWarps = 4;
 
 __host__ __device__ inline size_t warp_slice_doubles(int smax) {
-  // block + row scales, then 3 int arrays (idx, perm, iperm) packed in doubles
-  return size_t(smax) * lda_of(smax) + smax + (3 * size_t(smax) + 1) / 2;
+  // block + row scales, then 5 int arrays (idx, perm, iperm, rowoff, rowk0)
+  return size_t(smax) * lda_of(smax) + smax + (5 * size_t(smax) + 2) / 2;
 }
 
 __global__ void __launch_bounds__(32 * kFactorWarps) factor_warp_kernel(
@@ -281,25 +337,22 @@ __global__ void __launch_bounds__(32 * kFactorWarps) factor_warp_kernel(
     int* sidx = reinterpret_cast<int*>(rs + s);
     int* perm = sidx + s;
     int* iperm = perm + s;
+    int* rowoff = iperm + s;      // s + 1
+    int* rowk0 = rowoff + s + 1;  // s
     for (int i = lane; i < s; i += 32) {
-      sidx[i] = idx[base + i];
+      const int r = idx[base + i];
+      sidx[i] = r;
       perm[i] = i;
+      const int a = ptr[r];
+      rowk0[i] = a;
+      rowoff[i + 1] = ptr[r + 1] - a;
     }
     for (int e = lane; e < s * ld; e += 32) A[e] = 0.0;
     __syncwarp();
-    // 1. extraction: lane per block row, binary search of each CSR column
-    for (int i = lane; i < s; i += 32) {
-      const int row = sidx[i];
-      for (int k = ptr[row]; k < ptr[row + 1]; ++k) {
-        const int c = col[k];
-        int lo = 0, hi = s - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (sidx[mid] < c) lo = mid + 1; else hi = mid;
-        }
-        if (sidx[lo] == c) A[i * ld + lo] = val[k];
-      }
-    }
+    warp_scan_rows(lane, s, rowoff);
+    __syncwarp();
+    // 1. extraction: all (row, entry) pairs of the patch as independent items
+    extract_entries(lane, 32, s, ld, sidx, rowoff, rowk0, col, val, A);
     __syncwarp();
     // 2. row scales / all-zero-row guard
     int bad = 0;
