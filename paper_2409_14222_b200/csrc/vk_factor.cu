@@ -290,7 +290,7 @@ struct Bucket {
 };
 
 std::vector<Bucket> make_buckets(const std::vector<int64_t>& off, int first, int count) {
-  static const int edges[] = {16, 32, 48, 64, 80, 96, 112, 128, 144, kMaxPatch};
+  static const int edges[] = {16, 24, 32, 40, 48, 56, 64, 80, 96, 112, 128, 144, kMaxPatch};
   std::vector<Bucket> b(sizeof(edges) / sizeof(int));
   for (size_t i = 0; i < b.size(); ++i) b[i].smax = edges[i];
   for (int p = first; p < first + count; ++p) {
