@@ -118,25 +118,107 @@ class ClockSampler:
 # CPU reference arm / baseline (oracle = the reference algorithm restated)
 # ----------------------------------------------------------------------------
 
-def cpu_sweep_sample(pack, steps=3, warmup=1, sample=CPU_SAMPLE_PATCHES):
+_CPU = {}
+
+
+def _cpu_worker(w, lo, hi, conn):
+    """Forked worker owning patches [lo, hi): factor them once (reference
+    vanka.factor_patches), then on every "apply" write
+    out_w = sum_i R_i^T W_i A_i^-1 R_i r over its patches (reference
+    vanka.py:145-147, scipy getrs per patch) into its shared-memory row."""
+    import scipy.sparse as sp
+    from multiprocessing import shared_memory
+    from oracle import vanka_oracle as O
+    ps, n = _CPU["ps"], _CPU["n"]
+    a = sp.csr_matrix(_CPU["a"])
+    facs = {}
+    for j in range(lo, hi):
+        ii = ps.patch(j)
+        facs[j] = O.lu_factor(O.extract_submatrix(a, ii, ii))
+    shm = shared_memory.SharedMemory(name=_CPU["shm"])
+    buf = np.ndarray((_CPU["workers"] + 1, n), dtype=np.float64, buffer=shm.buf)
+    r, out = buf[-1], buf[w]
+    conn.send("ready")
+    while conn.recv() == "apply":
+        out[:] = 0.0
+        for j in range(lo, hi):
+            a_, b_ = ps.offsets[j], ps.offsets[j + 1]
+            ii = ps.indices[a_:b_]
+            out[ii] += ps.weights[a_:b_] * O.lu_solve(facs[j], r[ii])
+        conn.send("done")
+    del r, out, buf
+    shm.close()
+
+
+def cpu_sweep_sample(pack, steps=3, warmup=1, sample=None, workers=None):
+    """The reference algorithm (oracle port: scipy getrs per patch, weighted
+    scatter in patch order) on the host cores: the sampled patches are split
+    into contiguous slices, one forked worker process per core, partial sums
+    in shared memory added by the parent."""
+    import multiprocessing as mp
+    from multiprocessing import shared_memory
     from oracle import vanka_oracle as O
     lv = pack.fine
     ps = O.build_patches(lv.mixed, lv.system.bc)
-    O.factor_patches(ps, lv.system, limit=sample)
+    workers = workers or max(1, min(os.cpu_count() or 1, 64))
+    sample = min(ps.num_patches, sample or CPU_SAMPLE_PATCHES * workers)
     n = lv.system.matrix.shape[0]
-    r = np.random.default_rng(1).uniform(-1.0, 1.0, n)
-    for _ in range(warmup):
-        O.apply_additive(ps, r, limit=sample)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        O.apply_additive(ps, r, limit=sample)
-        times.append(time.perf_counter() - t0)
+    shm = shared_memory.SharedMemory(create=True, size=8 * (workers + 1) * n)
+    buf = np.ndarray((workers + 1, n), dtype=np.float64, buffer=shm.buf)
+    buf[-1] = np.random.default_rng(1).uniform(-1.0, 1.0, n)
+    _CPU.update(ps=ps, a=lv.system.matrix, shm=shm.name, n=n, workers=workers)
+    cuts = np.linspace(0, sample, workers + 1).astype(int)
+    env_threads = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS")}
+    os.environ.update(OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1")
+    ctx = mp.get_context("fork")
+    procs, conns = [], []
+    try:
+        for w in range(workers):
+            parent, child = ctx.Pipe()
+            p = ctx.Process(target=_cpu_worker, args=(w, int(cuts[w]), int(cuts[w + 1]), child),
+                            daemon=True)
+            p.start()
+            procs.append(p)
+            conns.append(parent)
+        for c in conns:
+            c.recv()                                   # factorised
+
+        def sweep():
+            for c in conns:
+                c.send("apply")
+            for c in conns:
+                c.recv()
+            return buf[:workers].sum(axis=0)
+
+        for _ in range(warmup):
+            sweep()
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            total = sweep()
+            times.append(time.perf_counter() - t0)
+        for c in conns:
+            c.send("stop")
+        for p in procs:
+            p.join(timeout=30)
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.terminate()
+        for k, v in env_threads.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        del buf
+        shm.close()
+        shm.unlink()
     t = statistics.median(times)
-    return {"value": sample / t, "unit": UNIT, "cores": 1, "kind": "port",
+    return {"value": sample / t, "unit": UNIT, "cores": workers, "kind": "port",
             "sample": f"first {sample} of {ps.num_patches} patches of the {CONFIG} finest "
-                      f"level, scipy getrs per patch (reference apply_additive loop), "
-                      f"median of {steps}", "ms_per_step": t * 1e3}
+                      f"level: the reference apply_additive loop (scipy getrs per patch) split "
+                      f"over {workers} forked worker processes, partial sums added; median of "
+                      f"{steps}", "ms_per_step": t * 1e3, "checksum": float(np.sum(total))}
 
 
 def run_reference(args):
@@ -320,7 +402,7 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu:
         cpu = cpu_sweep_sample(pack, steps=3, warmup=1)
-        cpu.pop("ms_per_step", None)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
