@@ -24,22 +24,12 @@ struct Csr {
   // CSR-stream schedule: row blocks of <= kStreamNnz nonzeros / kStreamRows rows
   int32_t nblocks = 0;
   int32_t* rowblk = nullptr;   // [nblocks+1]
-  // block-local column compression: per row block the sorted unique columns
-  // (ucol[ucolptr[b] .. ucolptr[b+1])) and a 16-bit local index per nonzero
-  int32_t* ucolptr = nullptr;  // [nblocks+1]
-  int32_t* ucol = nullptr;     // [sum of unique columns]
-  uint16_t* lidx = nullptr;    // [nnz] (+ 32 B slack for 16-byte bulk copies)
-  int64_t nucol = 0;
-  int32_t nlong = 0;           // rows longer than one block (sequential fallback kernel)
-  int32_t* longrows = nullptr;
-  int4* blkinfo = nullptr;     // per block {r0, nrows, k0, nnz}
-  int2* blkucol = nullptr;     // per block {u0, nu}
-  int32_t max_nu = 0, max_nr = 0;
 };
 
 constexpr int kStreamThreads = 256;
-constexpr int kStreamNnz = 2040;   // nonzeros per row block (<= 256 aligned groups of 8)
-constexpr int kStreamRows = 512;   // rows per row block
+constexpr int kStreamU = 8;
+constexpr int kStreamNnz = kStreamThreads * kStreamU;   // 2048 nonzeros per block
+constexpr int kStreamRows = 512;
 
 // Patch set: CSR-like layout of patch DoF lists + explicit inverses.
 struct Patches {
