@@ -82,7 +82,15 @@ def main():
                       args.reps, st)
         t_res = timed(lambda: L.call("vk_residual", A.handle, L.ptr(r), L.ptr(x), L.ptr(y), sp_),
                       args.reps, st)
+        # library reference point (not product code): cuSPARSE SpMV via torch
+        m = lv.system.matrix
+        tcsr = torch.sparse_csr_tensor(torch.from_numpy(m.indptr.astype(np.int32)).cuda(),
+                                       torch.from_numpy(m.indices.astype(np.int32)).cuda(),
+                                       torch.from_numpy(m.data).cuda(), size=m.shape)
+        t_cusp = timed(lambda: torch.mv(tcsr, x), args.reps, st)
+        del tcsr
         rec = {"N": N, "J": J, "nnz": int(A.nnz), "sum_s": s1, "sum_s2": s2, "smax": int(sz.max()),
+               "cusparse_spmv_ms": t_cusp,
                "build_s": t_build, "factor_s": t_factor, "factor_first_s": t_factor_first,
                "factor_gflops_lu_equiv": (2.0 / 3.0) * s3 / t_factor / 1e9,
                "solve_ms": t_solve, "accumulate_ms": t_acc, "residual_ms": t_res}
