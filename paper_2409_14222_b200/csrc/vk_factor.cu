@@ -448,6 +448,188 @@ __global__ void __launch_bounds__(32 * kFactorWarps) factor_warp_kernel(
   }
 }
 
+// Register-tiled Gauss-Jordan for s <= TR*RA (= TC*CB): a CTA of TR x TC
+// threads holds the whole block in registers, thread (tr, tc) owning rows
+// tr + TR*ra and columns tc + TC*cb.  Rows are never moved: LAPACK's row
+// interchanges are tracked as the position->row map `perm` (so the pivot
+// search, its lowest-position tie-break and the guard are those of getrf);
+// each step the owners publish the pivot column and the scaled pivot row in
+// double-buffered shared arrays and every thread applies the rank-1 update
+// to its tile with the same per-element arithmetic as factor_kernel.  The
+// inverse Ainv[i][j] = Y[perm[i]][iperm[j]] is scattered straight from the
+// registers to the column-major operator.
+template <int TR, int TC, int RA, int CB>
+__global__ void __launch_bounds__(TR * TC) factor_tile_kernel(
+    const int* __restrict__ plist, int count, const int64_t* __restrict__ off,
+    const int* __restrict__ idx, const int* __restrict__ ptr, const int* __restrict__ col,
+    const double* __restrict__ val, const int64_t* __restrict__ opoff, double* __restrict__ inv,
+    int* __restrict__ status) {
+  constexpr int NT = TR * TC;
+  constexpr int SM = TR * RA;              // largest block
+  static_assert(TC * CB == SM, "square tiling");
+  constexpr int LD = SM | 1;
+  __shared__ double A[SM * LD];
+  __shared__ double rs[SM];
+  __shared__ double colk[2][SM];
+  __shared__ double prow[2][SM];
+  __shared__ int sidx[SM], perm[SM], posof[SM], rowoff[SM + 1], rowk0[SM];
+  __shared__ int s_r, s_bad;
+  __shared__ double s_rinv;
+  const int t = threadIdx.x;
+  const int tr = t / TC, tc = t % TC;
+  const int lane = t & 31;
+
+  for (int bb = blockIdx.x; bb < count; bb += gridDim.x) {
+    const int p = plist[bb];
+    const int64_t base = off[p];
+    const int s = static_cast<int>(off[p + 1] - base);
+    const int ld = s | 1;
+    for (int i = t; i < s; i += NT) {
+      const int r = idx[base + i];
+      sidx[i] = r;
+      perm[i] = i;
+      const int a0 = ptr[r];
+      rowk0[i] = a0;
+      rowoff[i + 1] = ptr[r + 1] - a0;
+    }
+    for (int e = t; e < s * ld; e += NT) A[e] = 0.0;
+    if (t == 0) s_bad = 0;
+    __syncthreads();
+    if (t < 32) warp_scan_rows(lane, s, rowoff);
+    __syncthreads();
+    extract_entries(t, NT, s, ld, sidx, rowoff, rowk0, col, val, A);
+    __syncthreads();
+    for (int i = t; i < s; i += NT) {           // row scales, zero-row guard
+      double m = 0.0;
+      for (int j = 0; j < s; ++j) m = fmax(m, fabs(A[i * ld + j]));
+      rs[i] = m;
+      if (m == 0.0) s_bad = VK_PATCH_ZERO_ROW;
+    }
+    double a[RA][CB];
+#pragma unroll
+    for (int ra = 0; ra < RA; ++ra)
+#pragma unroll
+      for (int cb = 0; cb < CB; ++cb) {
+        const int i = tr + TR * ra, j = tc + TC * cb;
+        a[ra][cb] = (i < s && j < s) ? A[i * ld + j] : 0.0;
+      }
+    __syncthreads();
+    if (s_bad) {
+      if (t == 0) status[p] = s_bad;
+      __syncthreads();
+      continue;
+    }
+    int bad = 0;
+    for (int k = 0; k < s; ++k) {
+      const int buf = k & 1;
+      // publish pivot column k (owners: tc == k % TC)
+      if (tc == k % TC) {
+        const int kb = k / TC;
+#pragma unroll
+        for (int ra = 0; ra < RA; ++ra) {
+          const int i = tr + TR * ra;
+          double v = 0.0;
+#pragma unroll
+          for (int cb = 0; cb < CB; ++cb)
+            if (cb == kb) v = a[ra][cb];
+          if (i < s) colk[buf][i] = v;
+        }
+      }
+      __syncthreads();
+      if (t < 32) {                              // pivot search over positions k..s-1
+        double best = -1.0;
+        int bi = s;
+        for (int q = k + lane; q < s; q += 32) {
+          const double v = fabs(colk[buf][perm[q]]);
+          if (v > best) {
+            best = v;
+            bi = q;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+          }
+        }
+        if (lane == 0) {
+          const int tmp = perm[k];
+          perm[k] = perm[bi];
+          perm[bi] = tmp;
+          const int r = perm[k];
+          const double piv = colk[buf][r];
+          s_r = r;
+          if (!(fabs(piv) >= 1e-12 * rs[r])) {
+            s_bad = VK_PATCH_SMALL_PIVOT;
+          } else {
+            s_rinv = 1.0 / piv;
+          }
+        }
+      }
+      __syncthreads();
+      if (s_bad) {
+        bad = s_bad;
+        break;
+      }
+      const int r = s_r;
+      const double rinv = s_rinv;
+      // scaled pivot row (owners: tr == r % TR)
+      if (tr == r % TR) {
+        const int rb = r / TR;
+#pragma unroll
+        for (int ra = 0; ra < RA; ++ra) {
+          if (ra != rb) continue;
+#pragma unroll
+          for (int cb = 0; cb < CB; ++cb) {
+            const int j = tc + TC * cb;
+            const double v = (j == k) ? rinv : a[ra][cb] * rinv;
+            a[ra][cb] = v;
+            if (j < s) prow[buf][j] = v;
+          }
+        }
+      }
+      __syncthreads();
+      double pj[CB];
+#pragma unroll
+      for (int cb = 0; cb < CB; ++cb) {
+        const int j = tc + TC * cb;
+        pj[cb] = (j < s) ? prow[buf][j] : 0.0;
+      }
+#pragma unroll
+      for (int ra = 0; ra < RA; ++ra) {
+        const int i = tr + TR * ra;
+        if (i >= s || i == r) continue;
+        const double f = colk[buf][i];
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) {
+          const int j = tc + TC * cb;
+          a[ra][cb] = (j == k) ? -f * rinv : fma(-f, pj[cb], a[ra][cb]);
+        }
+      }
+    }
+    if (bad) {
+      if (t == 0) status[p] = bad;
+      __syncthreads();
+      continue;
+    }
+    for (int q = t; q < s; q += NT) posof[perm[q]] = q;
+    __syncthreads();
+    double* dst = inv + opoff[p];
+#pragma unroll
+    for (int ra = 0; ra < RA; ++ra)
+#pragma unroll
+      for (int cb = 0; cb < CB; ++cb) {
+        const int pr = tr + TR * ra, pc = tc + TC * cb;
+        if (pr < s && pc < s) dst[int64_t(perm[pc]) * s + posof[pr]] = a[ra][cb];
+      }
+    if (t == 0) status[p] = VK_PATCH_OK;
+    __syncthreads();
+  }
+}
+
 int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int* d_status,
                   double* blocks, const std::vector<int64_t>* blk_off_host, int extract_only,
                   cudaStream_t st) {
@@ -463,7 +645,20 @@ int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int
   }
   const size_t smem = factor_smem_bytes(bk.smax);
   const int count = static_cast<int>(bk.ids.size());
-  if (!extract_only && bk.smax <= 64) {
+  if (!extract_only && bk.smax <= 32) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_tile_kernel<8, 8, 4, 4>, 64, 0);
+    const int grid = std::max(1, std::min(count, 148 * std::max(per_sm, 1)));
+    factor_tile_kernel<8, 8, 4, 4><<<grid, 64, 0, st>>>(d_ids, count, h->off, h->idx, a->indptr,
+                                                       a->indices, a->data, h->opoff, h->inv, d_status);
+  } else if (!extract_only && bk.smax <= 64) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_tile_kernel<8, 16, 8, 4>, 128, 0);
+    const int grid = std::max(1, std::min(count, 148 * std::max(per_sm, 1)));
+    factor_tile_kernel<8, 16, 8, 4><<<grid, 128, 0, st>>>(d_ids, count, h->off, h->idx, a->indptr,
+                                                         a->indices, a->data, h->opoff, h->inv,
+                                                         d_status);
+  } else if (false) {
     const size_t wsm = sizeof(double) * warp_slice_doubles(bk.smax) * kFactorWarps;
     VK_CHECK_CUDA(cudaFuncSetAttribute(factor_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(wsm)));
