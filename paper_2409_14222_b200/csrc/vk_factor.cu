@@ -20,6 +20,8 @@
 // Size classes: patches are bucketed by size so each launch sizes its
 // dynamic shared memory (and occupancy) to the bucket's largest block.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "vk_common.cuh"
@@ -778,8 +780,31 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
   VK_CHECK_CUDA(cudaMemset(d_status, 0, sizeof(int) * std::max(h->npatch, 1)));
   auto buckets = make_buckets(h->h_off, 0, h->npatch);
   int st = VK_OK;
+  // VK_FACTOR_TIMING=1 prints the device time of every size-class launch
+  static const bool timing = getenv("VK_FACTOR_TIMING") != nullptr;
   for (auto& bk : buckets) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing && !bk.ids.empty()) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, 0);
+    }
     st = launch_bucket(bk, h, a, d_status, nullptr, nullptr, 0, 0);
+    if (e0) {
+      cudaEventRecord(e1, 0);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      double f = 0.0;
+      for (int q : bk.ids) {
+        const double sz = double(h->h_off[q + 1] - h->h_off[q]);
+        f += 2.0 * sz * sz * sz / 3.0;
+      }
+      fprintf(stderr, "[vk_factor] class <=%d: %zu patches, %.3f ms (incl. id upload), %.1f GFLOP/s LU-equiv\n",
+              bk.smax, bk.ids.size(), ms, f / (ms * 1e-3) / 1e9);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
     if (st) break;
   }
   std::vector<int32_t> hs(h->npatch);
