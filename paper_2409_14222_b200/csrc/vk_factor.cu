@@ -469,8 +469,7 @@ __global__ void __launch_bounds__(TR * TC) factor_tile_kernel(
   constexpr int NT = TR * TC;
   constexpr int SM = TR * RA;              // largest block
   static_assert(TC * CB == SM, "square tiling");
-  constexpr int LD = SM | 1;
-  __shared__ double A[SM * LD];
+  extern __shared__ __align__(16) double A[];   // SM x (SM|1) extraction staging
   __shared__ double rs[SM];
   __shared__ double colk[2][SM];
   __shared__ double prow[2][SM];
@@ -647,19 +646,38 @@ int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int
   }
   const size_t smem = factor_smem_bytes(bk.smax);
   const int count = static_cast<int>(bk.ids.size());
-  if (!extract_only && bk.smax <= 32) {
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_tile_kernel<8, 8, 4, 4>, 64, 0);
-    const int grid = std::max(1, std::min(count, 148 * std::max(per_sm, 1)));
-    factor_tile_kernel<8, 8, 4, 4><<<grid, 64, 0, st>>>(d_ids, count, h->off, h->idx, a->indptr,
-                                                       a->indices, a->data, h->opoff, h->inv, d_status);
-  } else if (!extract_only && bk.smax <= 64) {
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_tile_kernel<8, 16, 8, 4>, 128, 0);
-    const int grid = std::max(1, std::min(count, 148 * std::max(per_sm, 1)));
-    factor_tile_kernel<8, 16, 8, 4><<<grid, 128, 0, st>>>(d_ids, count, h->off, h->idx, a->indptr,
-                                                         a->indices, a->data, h->opoff, h->inv,
-                                                         d_status);
+  if (!extract_only && bk.smax <= 128) {
+    // register-tiled classes: (TR x TC threads, RA x CB tile per thread)
+    cudaError_t e = cudaSuccess;
+#define VK_TILE(TR_, TC_, RA_, CB_)                                                              \
+  do {                                                                                         \
+    auto kern = factor_tile_kernel<TR_, TC_, RA_, CB_>;                                        \
+    const size_t dsm = sizeof(double) * size_t(TR_ * RA_) * size_t((TR_ * RA_) | 1);          \
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));    \
+    int per_sm = 1;                                                                            \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TR_ * TC_, dsm);              \
+    const int grid = std::max(1, std::min(count, 148 * std::max(per_sm, 1)));                 \
+    if (e == cudaSuccess)                                                                      \
+      kern<<<grid, TR_ * TC_, dsm, st>>>(d_ids, count, h->off, h->idx, a->indptr, a->indices,  \
+                                         a->data, h->opoff, h->inv, d_status);                 \
+  } while (0)
+    if (bk.smax <= 16) VK_TILE(8, 8, 2, 2);
+    else if (bk.smax <= 24) VK_TILE(8, 8, 3, 3);
+    else if (bk.smax <= 32) VK_TILE(8, 8, 4, 4);
+    else if (bk.smax <= 40) VK_TILE(8, 8, 5, 5);
+    else if (bk.smax <= 48) VK_TILE(8, 8, 6, 6);
+    else if (bk.smax <= 56) VK_TILE(8, 8, 7, 7);
+    else if (bk.smax <= 64) VK_TILE(8, 16, 8, 4);
+    else if (bk.smax <= 80) VK_TILE(16, 16, 5, 5);
+    else if (bk.smax <= 96) VK_TILE(16, 16, 6, 6);
+    else if (bk.smax <= 112) VK_TILE(16, 16, 7, 7);
+    else VK_TILE(16, 16, 8, 8);
+#undef VK_TILE
+    if (e != cudaSuccess) {
+      cudaFree(d_ids);
+      vk::set_error("factor_tile_kernel: %s", cudaGetErrorString(e));
+      return VK_ERR_CUDA;
+    }
   } else if (false) {
     const size_t wsm = sizeof(double) * warp_slice_doubles(bk.smax) * kFactorWarps;
     VK_CHECK_CUDA(cudaFuncSetAttribute(factor_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
