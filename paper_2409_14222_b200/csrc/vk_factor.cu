@@ -17,8 +17,9 @@
 //      its source row (VK_PATCH_SMALL_PIVOT) exactly like sparsela.py:79-83.
 //   4. the explicit inverse (same bytes as L\U, no triangular dependency at
 //      apply time) is written column-major with the column permutation undone.
-// Size classes: patches are bucketed by size so each launch sizes its
-// dynamic shared memory (and occupancy) to the bucket's largest block.
+// Size classes: patches are bucketed by size; classes up to 128 run the
+// register-tiled kernel (factor_tile_kernel), larger ones the shared-memory
+// kernel (factor_kernel, also used for the extraction-only export).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -306,150 +307,6 @@ std::vector<Bucket> make_buckets(const std::vector<int64_t>& off, int first, int
   return b;
 }
 
-// Small patches (s <= 64): one WARP per patch, several independent patches per
-// CTA (no block barriers; only __syncwarp).  Same algorithm and arithmetic
-// as factor_kernel: verbatim extraction, row-scale guard, Gauss-Jordan with
-// LAPACK-order partial pivoting and the reference pivot test, column-major
-// inverse with the column permutation undone.  Lane j keeps pivot-row
-// entries j and j+32 in registers during each elimination step.
-constexpr int kFactorWarps = 4;
-
-__host__ __device__ inline size_t warp_slice_doubles(int smax) {
-  // block + row scales, then 5 int arrays (idx, perm, iperm, rowoff, rowk0)
-  return size_t(smax) * lda_of(smax) + smax + (5 * size_t(smax) + 2) / 2;
-}
-
-__global__ void __launch_bounds__(32 * kFactorWarps) factor_warp_kernel(
-    const int* __restrict__ plist, int count, int smax, const int64_t* __restrict__ off,
-    const int* __restrict__ idx, const int* __restrict__ ptr, const int* __restrict__ col,
-    const double* __restrict__ val, const int64_t* __restrict__ opoff, double* __restrict__ inv,
-    int* __restrict__ status) {
-  extern __shared__ __align__(16) double smem[];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  double* A = smem + warp * warp_slice_doubles(smax);
-  const int gw = blockIdx.x * kFactorWarps + warp;
-  const int nw = gridDim.x * kFactorWarps;
-  for (int b = gw; b < count; b += nw) {
-    const int p = plist[b];
-    const int64_t base = off[p];
-    const int s = static_cast<int>(off[p + 1] - base);
-    const int ld = lda_of(s);
-    double* rs = A + size_t(s) * ld;
-    int* sidx = reinterpret_cast<int*>(rs + s);
-    int* perm = sidx + s;
-    int* iperm = perm + s;
-    int* rowoff = iperm + s;      // s + 1
-    int* rowk0 = rowoff + s + 1;  // s
-    for (int i = lane; i < s; i += 32) {
-      const int r = idx[base + i];
-      sidx[i] = r;
-      perm[i] = i;
-      const int a = ptr[r];
-      rowk0[i] = a;
-      rowoff[i + 1] = ptr[r + 1] - a;
-    }
-    for (int e = lane; e < s * ld; e += 32) A[e] = 0.0;
-    __syncwarp();
-    warp_scan_rows(lane, s, rowoff);
-    __syncwarp();
-    // 1. extraction: all (row, entry) pairs of the patch as independent items
-    extract_entries(lane, 32, s, ld, sidx, rowoff, rowk0, col, val, A);
-    __syncwarp();
-    // 2. row scales / all-zero-row guard
-    int bad = 0;
-    for (int i = lane; i < s; i += 32) {
-      double m = 0.0;
-      for (int j = 0; j < s; ++j) m = fmax(m, fabs(A[i * ld + j]));
-      rs[i] = m;
-      if (m == 0.0) bad = 1;
-    }
-    if (__any_sync(0xffffffffu, bad)) {
-      if (lane == 0) status[p] = VK_PATCH_ZERO_ROW;
-      __syncwarp();
-      continue;
-    }
-    __syncwarp();
-    // 3. Gauss-Jordan with partial pivoting; lanes own rows (lane, lane+32)
-    //    and sweep the columns, reading the scaled pivot row as broadcasts
-    int st = VK_PATCH_OK;
-    const int i0 = lane, i1 = lane + 32;
-    for (int k = 0; k < s; ++k) {
-      double best = -1.0;
-      int bi = s;
-      for (int i = k + lane; i < s; i += 32) {
-        const double v = fabs(A[i * ld + k]);
-        if (v > best) {
-          best = v;
-          bi = i;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) {
-          best = ob;
-          bi = oi;
-        }
-      }
-      if (bi != k) {
-        for (int j = lane; j < s; j += 32) {
-          const double t = A[k * ld + j];
-          A[k * ld + j] = A[bi * ld + j];
-          A[bi * ld + j] = t;
-        }
-        if (lane == 0) {
-          const int t = perm[k];
-          perm[k] = perm[bi];
-          perm[bi] = t;
-        }
-      }
-      __syncwarp();
-      const double piv = A[k * ld + k];
-      if (!(fabs(piv) >= 1e-12 * rs[perm[k]])) {   // warp-uniform
-        st = VK_PATCH_SMALL_PIVOT;
-        break;
-      }
-      const double rinv = 1.0 / piv;
-      const bool u0 = i0 < s && i0 != k, u1 = i1 < s && i1 != k;
-      const double f0 = u0 ? A[i0 * ld + k] : 0.0;
-      const double f1 = u1 ? A[i1 * ld + k] : 0.0;
-      __syncwarp();                     // column k read before row k is scaled
-      for (int j = lane; j < s; j += 32)
-        A[k * ld + j] = (j == k) ? rinv : A[k * ld + j] * rinv;
-      __syncwarp();
-#pragma unroll 4
-      for (int j = 0; j < s; ++j) {
-        const double pj = A[k * ld + j];              // broadcast
-        if (j == k) {
-          if (u0) A[i0 * ld + k] = -f0 * rinv;
-          if (u1) A[i1 * ld + k] = -f1 * rinv;
-        } else {
-          if (u0) A[i0 * ld + j] = fma(-f0, pj, A[i0 * ld + j]);
-          if (u1) A[i1 * ld + j] = fma(-f1, pj, A[i1 * ld + j]);
-        }
-      }
-      __syncwarp();
-    }
-    if (st != VK_PATCH_OK) {
-      if (lane == 0) status[p] = st;
-      __syncwarp();
-      continue;
-    }
-    // 4. Ainv[i][j] = X[i][iperm[j]], written column-major
-    for (int q = lane; q < s; q += 32) iperm[perm[q]] = q;
-    __syncwarp();
-    double* dst = inv + opoff[p];
-    for (int e = lane; e < s * s; e += 32) {
-      const int j = e / s, i = e - j * s;
-      dst[e] = A[i * ld + iperm[j]];
-    }
-    if (lane == 0) status[p] = VK_PATCH_OK;
-    __syncwarp();
-  }
-}
-
 // Register-tiled Gauss-Jordan for s <= TR*RA (= TC*CB): a CTA of TR x TC
 // threads holds the whole block in registers, thread (tr, tc) owning rows
 // tr + TR*ra and columns tc + TC*cb.  Rows are never moved: LAPACK's row
@@ -678,17 +535,6 @@ int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int
       vk::set_error("factor_tile_kernel: %s", cudaGetErrorString(e));
       return VK_ERR_CUDA;
     }
-  } else if (false) {
-    const size_t wsm = sizeof(double) * warp_slice_doubles(bk.smax) * kFactorWarps;
-    VK_CHECK_CUDA(cudaFuncSetAttribute(factor_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(wsm)));
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, factor_warp_kernel, 32 * kFactorWarps, wsm);
-    const int grid = std::max(1, std::min((count + kFactorWarps - 1) / kFactorWarps,
-                                          148 * std::max(per_sm, 1)));
-    factor_warp_kernel<<<grid, 32 * kFactorWarps, wsm, st>>>(d_ids, count, bk.smax, h->off, h->idx,
-                                                            a->indptr, a->indices, a->data, h->opoff,
-                                                            h->inv, d_status);
   } else if (bk.smax <= 32) {
     VK_CHECK_CUDA(cudaFuncSetAttribute(factor_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(smem)));
