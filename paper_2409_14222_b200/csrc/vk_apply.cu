@@ -178,12 +178,101 @@ static int check_apply(vk_patches_t h) {
   return VK_OK;
 }
 
+namespace {
+
+// Small patch sets (coarse MG levels: fewer patches than resident warps) are
+// latency-bound in patch_solve_kernel — one warp streams a whole operator.
+// Here G warps of a CTA share one patch, warp g streaming columns
+// [g*cs, (g+1)*cs) for all rows; the G partial products are added in the
+// fixed order g = 0..G-1 (deterministic) before the weighting.
+template <int R, int G>
+__global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_split_kernel(
+    int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
+    const double* __restrict__ w, const int64_t* __restrict__ opoff,
+    const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
+  constexpr int PPC = kApplyWarps / G;               // patches per CTA
+  __shared__ double rsh[PPC][32 * R];
+  __shared__ double part[PPC][G][32 * R];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int slot = warp / G, g = warp % G;
+  for (int p0 = blockIdx.x * PPC; p0 < npatch; p0 += gridDim.x * PPC) {
+    const int p = p0 + slot;
+    const bool live = p < npatch;
+    int64_t base = 0, ob = 0;
+    int s = 0;
+    if (live) {
+      base = off[p];
+      s = static_cast<int>(off[p + 1] - base);
+      ob = opoff[p];
+      for (int i = g * 32 + lane; i < s; i += 32 * G) rsh[slot][i] = __ldg(r + idx[base + i]);
+    }
+    __syncthreads();
+    double y[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) y[q] = 0.0;
+    if (live) {
+      const int cs = (s + G - 1) / G;
+      const int j0 = g * cs, j1 = min(s, j0 + cs);
+      const double* A = inv + ob;
+      for (int j = j0; j < j1; j += 4) {
+        double a[4][R];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int q = 0; q < R; ++q) {
+            const int i = lane + 32 * q;
+            a[u][q] = (i < s && j + u < j1) ? __ldcs(A + (j + u) * s + i) : 0.0;
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double rj = (j + u < j1) ? rsh[slot][j + u] : 0.0;
+#pragma unroll
+          for (int q = 0; q < R; ++q) y[q] = fma(a[u][q], rj, y[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < R; ++q) part[slot][g][lane + 32 * q] = y[q];
+    }
+    __syncthreads();
+    if (live && g == 0) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = lane + 32 * q;
+        if (i < s) {
+          double acc = part[slot][0][i];
+#pragma unroll
+          for (int gg = 1; gg < G; ++gg) acc = __dadd_rn(acc, part[slot][gg][i]);
+          z[base + i] = __dmul_rn(w[base + i], acc);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
 extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
   if (int st = check_apply(h)) return st;
   VK_REQUIRE(r, "vk_patches_solve: null residual");
-  if (h->npatch > 0) {
+  const int rpl = (h->smax + 31) / 32;
+  if (h->npatch > 0 && h->npatch < 148 * kApplyWarps * 4 && rpl <= 4) {
+    // coarse levels: 4 warps per patch
+    constexpr int G = 4;
+    const int grid = std::min((h->npatch + kApplyWarps / G - 1) / (kApplyWarps / G), 148 * 16);
+#define VK_SPLIT(RV)                                                                        \
+  patch_solve_split_kernel<RV, G><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(        \
+      h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf)
+    switch (rpl) {
+      case 1: VK_SPLIT(1); break;
+      case 2: VK_SPLIT(2); break;
+      case 3: VK_SPLIT(3); break;
+      default: VK_SPLIT(4); break;
+    }
+#undef VK_SPLIT
+  } else if (h->npatch > 0) {
     const int grid = std::min((h->npatch + kApplyWarps - 1) / kApplyWarps, 148 * 8);
-    const int rpl = (h->smax + 31) / 32;
 #define VK_SOLVE(RV)                                                                        \
   if (h->mixed_sizes)                                                                       \
     patch_solve_kernel<RV, true><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(         \
