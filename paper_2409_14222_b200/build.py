@@ -47,6 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
              "-fvisibility=hidden", "--expt-relaxed-constexpr", *ARCH]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    flags += os.environ.get("VK_NVCC_FLAGS", "").split()  # experiments only
     for src in SOURCES:
         obj = os.path.join(tmp, src.replace(".cu", ".o"))
         cmd = [nvcc(), *flags, "-c", os.path.join(CSRC, src), "-o", obj]

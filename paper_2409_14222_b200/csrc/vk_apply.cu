@@ -67,8 +67,15 @@ __device__ __forceinline__ void stream_patch(int lane, int s, int64_t base,
 // only then streams patch p's operator.
 __host__ __device__ constexpr int unroll_of(int r) { return r <= 2 ? 8 : (r <= 4 ? 4 : 2); }
 
+// MINB: resident CTAs per SM the register allocation must allow (memory
+// parallelism: each warp keeps U*R column loads in flight).
+#ifndef VK_APPLY_MINB12
+#define VK_APPLY_MINB12 4
+#endif
+__host__ __device__ constexpr int minb_of(int r) { return r <= 2 ? VK_APPLY_MINB12 : (r <= 4 ? 3 : 2); }
+
 template <int RMAX, bool DISPATCH>
-__global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_kernel(
+__global__ void __launch_bounds__(kApplyWarps * 32, minb_of(RMAX)) patch_solve_kernel(
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
@@ -272,14 +279,20 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
     }
 #undef VK_SPLIT
   } else if (h->npatch > 0) {
-    const int grid = std::min((h->npatch + kApplyWarps - 1) / kApplyWarps, 148 * 8);
+    // persistent: exactly the resident CTAs, so no partial last wave
+    const int want = (h->npatch + kApplyWarps - 1) / kApplyWarps;
 #define VK_SOLVE(RV)                                                                        \
-  if (h->mixed_sizes)                                                                       \
-    patch_solve_kernel<RV, true><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(         \
+  if (h->mixed_sizes) {                                                                     \
+    auto k = patch_solve_kernel<RV, true>;                                                  \
+    const int grid = std::min(want, vk_resident_blocks((const void*)k, kApplyWarps * 32));  \
+    k<<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(                                    \
         h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf);                     \
-  else                                                                                      \
-    patch_solve_kernel<RV, false><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(        \
-        h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf)
+  } else {                                                                                  \
+    auto k = patch_solve_kernel<RV, false>;                                                 \
+    const int grid = std::min(want, vk_resident_blocks((const void*)k, kApplyWarps * 32));  \
+    k<<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(                                    \
+        h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf);                     \
+  }
     switch (rpl) {
       case 1: VK_SOLVE(1); break;
       case 2: VK_SOLVE(2); break;

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/vanka_b200.h"
@@ -97,4 +99,24 @@ static inline int vk_grid(int64_t work, int block, int cap = 148 * 16) {
   if (g < 1) g = 1;
   if (g > cap) g = cap;
   return static_cast<int>(g);
+}
+
+// Blocks of `kernel` that are resident on the whole device at once (SM count
+// x occupancy), cached per kernel.  Persistent grid-stride kernels launch
+// exactly this many so there is no partial last wave.
+static inline int vk_resident_blocks(const void* kernel, int block, size_t smem = 0) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(kernel);
+  if (it != cache.end()) return it->second;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int n = per_sm * sms;
+  cache.emplace(kernel, n);
+  return n;
 }
