@@ -89,10 +89,26 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
         carry = s;
       }
     } else {
-      for (int i = t; i < nr; i += kStreamThreads) {
-        const int a = sptr[i] - kc, e = sptr[i + 1] - kc;
+      // One thread per row.  Lane l starts d = (a - l) mod 16 steps late, so
+      // at every step the half-warp reads 16 distinct 8-byte bank slots
+      // ((a + k) mod 16 == (step + l) mod 16) instead of colliding whenever
+      // row starts agree mod 16; each row is still summed left to right.
+      for (int i0 = 0; i0 < nr; i0 += kStreamThreads) {
+        const int i = i0 + t;
+        int a = 0, len = 0, d = 0;
+        if (i < nr) {
+          a = sptr[i] - kc;
+          len = sptr[i + 1] - kc - a;
+          d = (a - (t & 31)) & 15;
+        }
+        const int steps = __reduce_max_sync(0xffffffffu, len > 0 ? len + d : 0);
         double s = 0.0;
-        for (int k = a; k < e; ++k) s = __dadd_rn(s, prod[k]);
+#pragma unroll 4
+        for (int q = 0; q < steps; ++q) {
+          const int k = q - d;
+          if (k >= 0 && k < len) s = __dadd_rn(s, prod[a + k]);
+        }
+        if (i >= nr) continue;
         const int row = r0 + i;
         if (MODE == 1) {
           y[row] = __dsub_rn(b[row], s);
