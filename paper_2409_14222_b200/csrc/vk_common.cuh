@@ -28,10 +28,16 @@ struct Csr {
   int32_t* rowblk = nullptr;   // [nblocks+1]
 };
 
-constexpr int kStreamThreads = 256;
-constexpr int kStreamU = 8;
+#ifndef VK_STREAM_THREADS
+#define VK_STREAM_THREADS 256
+#endif
+#ifndef VK_STREAM_U
+#define VK_STREAM_U 8
+#endif
+constexpr int kStreamThreads = VK_STREAM_THREADS;
+constexpr int kStreamU = VK_STREAM_U;
 constexpr int kStreamNnz = kStreamThreads * kStreamU;   // 2048 nonzeros per block
-constexpr int kStreamRows = 512;
+constexpr int kStreamRows = 2 * kStreamThreads;
 
 // Patch set: CSR-like layout of patch DoF lists + explicit inverses.
 struct Patches {
