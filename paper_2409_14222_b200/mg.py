@@ -25,8 +25,9 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib as L
-from .sparsela import DeviceCSR, device_csr, to_device, to_host, _device_operator
-from .vanka import build_patches, factor_patches
+from .sparsela import (DeviceCSR, device_csr, estimate_lambda_max, to_device, to_host,
+                       _device_operator)
+from .vanka import apply_additive, build_patches, factor_patches
 
 COARSE_CELLS_PER_SIDE = 5          # reference mg.py:28 (setup is not rebuilt here)
 LAMBDA_LOWER_FRACTION = 0.25       # reference mg.py:29
@@ -335,15 +336,44 @@ def _build(levels_in, nu, weighting, cheb_mode, damping_for, config=None):
     return MgHierarchy(levels, transfers, q, config, nu=nu, cheb_mode=cheb_mode)
 
 
+def estimate_spectra(hier: MgHierarchy, *, est_steps: int = 10, seed: int = 0) -> MgHierarchy:
+    """Chebyshev bounds of every relaxed level from the patch-preconditioned
+    operator, on the device (reference ``mg.build_hierarchy``, ``mg.py:
+    214-221``): lam_i = estimate_lambda_max(v -> A_i apply_additive(v),
+    m=est_steps, seed=seed + 31 i); ``level.cheb = ChebyshevParams(lam_i,
+    est_steps, seed + 31 i)``.  Cached V-cycle graphs are dropped (the
+    damping is baked into them)."""
+    import torch
+    for i, level in enumerate(hier.levels):
+        if level.patches is None:
+            continue
+        tmp = torch.empty(level.n, dtype=torch.float64, device="cuda")
+
+        def op(v, lv=level, t=tmp):
+            apply_additive(lv.patches, v, t)
+            return lv.A.matvec(t)
+        op._device = True
+        lam = estimate_lambda_max(op, m=est_steps, seed=seed + 31 * i, n=level.n)
+        level.cheb = ChebyshevParams(lam, est_steps, seed + 31 * i)
+    hier._graphs = {}
+    return hier
+
+
 def hierarchy_from_pack(pack, *, nu=2, weighting="invmult", cheb_mode="repeat",
-                        damping=0.5) -> MgHierarchy:
+                        damping=0.5, est_steps=10, seed=0) -> MgHierarchy:
     """Device hierarchy from a problem pack (assembled operators of every
     level, coarsest first).  ``damping`` pins damp = 2/(lower+upper) like the
-    BASELINE recipe (lower=1, upper=2/damping-1)."""
+    BASELINE recipe (lower=1, upper=2/damping-1); ``damping=None`` keeps the
+    reference's own bounds instead, estimated on the device
+    (:func:`estimate_spectra`, ``est_steps``/``seed`` as in
+    ``mg.build_hierarchy``)."""
     if cheb_mode not in CHEB_MODES:
         raise ValueError(f"unknown chebyshev mode {cheb_mode!r}")
-    upper = 2.0 / damping - 1.0
     lv = [(pl.mixed, pl.system, pl.prolong, None) for pl in pack.levels]
+    if damping is None:
+        hier = _build(lv, nu, weighting, cheb_mode, lambda i: None)
+        return estimate_spectra(hier, est_steps=est_steps, seed=seed)
+    upper = 2.0 / damping - 1.0
     return _build(lv, nu, weighting, cheb_mode,
                   lambda i: FixedDamping(1.0, upper) if i > 0 else None)
 

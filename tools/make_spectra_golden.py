@@ -1,0 +1,93 @@
+#!/usr/bin/env python
+"""Golden Chebyshev spectra + MG-FGMRES histories with the reference's OWN
+default smoother bounds (build container only: imports the unmodified
+reference from /root/reference).
+
+For each small MG case the reference hierarchy is built exactly as
+``stokesmg.mg.build_hierarchy(case, k, R, nu=2, cheb_mode=mode,
+est_steps=10, seed=0)`` (``mg.py:177-233``): every non-coarse level's
+``ChebyshevParams.lam`` comes from ``estimate_lambda_max`` (``sparsela.py:
+194-226``) on A * apply_additive with seed ``31 * i`` (``mg.py:214-221``).
+Recorded per case: the per-level lam, and the FGMRES(30) residual history /
+iterations for the same RHS as ``make_packs.py`` (seeded uniform velocity
+load).  The operators themselves are the committed packs (same assembly).
+
+    python tools/make_spectra_golden.py            # writes tests/golden/*_spectra.json
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, HERE)
+sys.path.insert(0, ROOT)
+
+from make_packs import CASES, _ref  # noqa: E402
+
+# (case name, chebyshev mode)
+RUNS = [("s_thtri2", "repeat"), ("s_thtri4", "repeat"), ("s_thquad3", "repeat"),
+        ("s_thquad2", "repeat"), ("s_bdm3", "repeat"), ("s_rt2", "repeat"),
+        ("s_thtri2", "degree"), ("s_bdm3", "degree")]
+EST_STEPS = 10
+SEED = 0
+
+
+def run(name, mode):
+    _ref()
+    import stokesmg.mg as mg
+    from stokesmg.sparsela import fgmres, nullspace_projector
+
+    case, k, coarse, refinements = CASES[name]
+    mg.COARSE_CELLS_PER_SIDE = coarse
+    t0 = time.perf_counter()
+    hier = mg.build_hierarchy(case, k, refinements, nu=2, cheb_mode=mode,
+                              est_steps=EST_STEPS, seed=SEED)
+    t_setup = time.perf_counter() - t0
+    lams = [None] + [float(lv.cheb.lam) for lv in hier.levels[1:]]
+
+    fine = hier.fine
+    a = fine.system.matrix
+    nvel = fine.system.num_velocity
+    b = np.zeros(a.shape[0])
+    b[:nvel] = np.random.default_rng(0).uniform(-1.0, 1.0, nvel)
+    b[fine.system.bc.indices] = 0.0
+    nsp = nullspace_projector([mg.pressure_kernel(fine.mixed)])
+    prec = mg.make_preconditioner(hier)
+    pb = nsp(b.copy())
+    x, base, hist, its, conv = None, None, [], 0, False
+    for _ in range(20):
+        x, rep = fgmres(a, b, preconditioner=prec, rtol=1e-8, max_it=30,
+                        nullspace=nsp, x0=x, target_norm=base)
+        if base is None:
+            base = float(np.linalg.norm(pb))
+            hist.extend(rep.history.tolist())
+        else:
+            hist.extend(rep.history[1:].tolist())
+        its += rep.iterations
+        if rep.converged:
+            conv = True
+            break
+    return {"name": name, "mode": mode, "est_steps": EST_STEPS, "seed": SEED,
+            "lam": lams, "iterations": its, "converged": conv, "history": hist,
+            "setup_s": t_setup}
+
+
+def main():
+    out = os.path.join(ROOT, "tests", "golden")
+    for name, mode in RUNS:
+        rec = run(name, mode)
+        path = os.path.join(out, f"{name}_{mode}_spectra.json")
+        with open(path, "w") as fh:
+            json.dump(rec, fh, indent=1)
+        print(f"{name} {mode}: lam={rec['lam']} its={rec['iterations']}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
