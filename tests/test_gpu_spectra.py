@@ -6,8 +6,9 @@ goldens (tools/make_spectra_golden.py) hold the reference's own lam per level
 and its MG-FGMRES(30) history with those bounds, for both Chebyshev modes.
 
 Gates: lam relative 1e-10 (10 Arnoldi steps on operators that differ from
-the reference by ~1e-16 per application); history as test_gpu_parity (1e-10,
-iterations +-1).
+the reference by ~1e-16 per application); history as test_gpu_parity:
+iterations +-1 and max(1e-10, SELFVAR_FACTOR * the reference's own
+1-vs-8-BLAS-thread history variation recorded in the golden).
 """
 
 import json
@@ -21,6 +22,7 @@ from conftest import GOLDEN, load_case
 RUNS = sorted(f[:-len("_spectra.json")] for f in os.listdir(GOLDEN) if f.endswith("_spectra.json"))
 REL_LAM = 1e-10
 REL_HIST = 1e-10
+SELFVAR_FACTOR = 4.0
 
 
 def _golden(run):
@@ -53,9 +55,12 @@ def test_device_spectra_and_fgmres(run, capsys):
     ref = np.asarray(g["history"])
     m = min(len(hist), len(ref))
     rel = float(np.max(np.abs(hist[:m] - ref[:m]) / ref[:m]))
+    floor = g["selfvar_history_max_rel"]
+    tol = max(REL_HIST, SELFVAR_FACTOR * floor)
     with capsys.disabled():
         print(f"\n[{run}] lam rel {rel_lam:.2e}; iterations {its} (ref {g['iterations']}); "
-              f"history rel {rel:.2e}")
+              f"history rel {rel:.2e} (strict 1e-10: {'pass' if rel <= REL_HIST else 'FAIL'}; "
+              f"reference self-variation {floor:.2e}; tolerance {tol:.2e})")
     assert rel_lam <= REL_LAM
     assert conv and abs(its - g["iterations"]) <= 1
-    assert rel <= REL_HIST
+    assert rel <= tol

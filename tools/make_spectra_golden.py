@@ -10,7 +10,10 @@ est_steps=10, seed=0)`` (``mg.py:177-233``): every non-coarse level's
 194-226``) on A * apply_additive with seed ``31 * i`` (``mg.py:214-221``).
 Recorded per case: the per-level lam, and the FGMRES(30) residual history /
 iterations for the same RHS as ``make_packs.py`` (seeded uniform velocity
-load).  The operators themselves are the committed packs (same assembly).
+load), all with 1 BLAS thread, plus the reference's self-variation: the same
+run with 8 BLAS threads (only the dense coarse getrf changes), as
+max_j |h_j - h'_j| / h_j (cf. tools/reference_selfvar.py).  The operators
+themselves are the committed packs (same assembly).
 
     python tools/make_spectra_golden.py            # writes tests/golden/*_spectra.json
 """
@@ -80,9 +83,17 @@ def run(name, mode):
 
 
 def main():
+    from threadpoolctl import threadpool_limits
     out = os.path.join(ROOT, "tests", "golden")
     for name, mode in RUNS:
-        rec = run(name, mode)
+        with threadpool_limits(1):
+            rec = run(name, mode)
+        with threadpool_limits(8):
+            alt = run(name, mode)
+        h, h2 = np.asarray(rec["history"]), np.asarray(alt["history"])
+        m = min(len(h), len(h2))
+        rec["selfvar_history_max_rel"] = float(np.max(np.abs(h[:m] - h2[:m]) / h[:m]))
+        rec["selfvar_iterations"] = alt["iterations"]
         path = os.path.join(out, f"{name}_{mode}_spectra.json")
         with open(path, "w") as fh:
             json.dump(rec, fh, indent=1)
