@@ -311,31 +311,44 @@ std::vector<Bucket> make_buckets(const std::vector<int64_t>& off, int first, int
 // threads holds the whole block in registers, thread (tr, tc) owning rows
 // tr + TR*ra and columns tc + TC*cb.  Rows are never moved: LAPACK's row
 // interchanges are tracked as the position->row map `perm` (so the pivot
-// search, its lowest-position tie-break and the guard are those of getrf);
-// each step the owners publish the pivot column and the scaled pivot row in
-// double-buffered shared arrays and every thread applies the rank-1 update
-// to its tile with the same per-element arithmetic as factor_kernel.  The
-// inverse Ainv[i][j] = Y[perm[i]][iperm[j]] is scattered straight from the
-// registers to the column-major operator.
-template <int TR, int TC, int RA, int CB>
-__global__ void __launch_bounds__(TR * TC) factor_tile_kernel(
+// search, its lowest-position tie-break and the guard are those of getrf).
+//
+// Step k (two CTA barriers):
+//   * every warp runs the pivot search over positions k..s-1 of the
+//     published column k itself (redux.sync argmax, lowest position on ties)
+//     and swaps its own copy of `perm` -- no barrier between search and use;
+//   * the owners of the pivot row scale it in registers and publish it;
+//     barrier;
+//   * every thread applies the rank-1 update to its tile; the owners of
+//     column k+1 publish it for the next search; barrier.
+// The column loop is split as k = kb*TC + kt with kb unrolled, so the pivot
+// column's register block index is a compile-time constant (no select chains
+// over the tile).  Per-element arithmetic is unchanged: row scaling
+// a*rinv (rinv in the pivot column), update fma(-f, p_j, a) (-f*rinv in the
+// pivot column).  The inverse Ainv[i][j] = Y[perm[i]][iperm[j]] is scattered
+// straight from the registers to the column-major operator.
+template <int TR, int TC, int RA, int CB, int MB>
+__global__ void __launch_bounds__(TR * TC, MB) factor_tile_kernel(
     const int* __restrict__ plist, int count, const int64_t* __restrict__ off,
     const int* __restrict__ idx, const int* __restrict__ ptr, const int* __restrict__ col,
     const double* __restrict__ val, const int64_t* __restrict__ opoff, double* __restrict__ inv,
     int* __restrict__ status) {
   constexpr int NT = TR * TC;
+  constexpr int NW = NT / 32;
   constexpr int SM = TR * RA;              // largest block
   static_assert(TC * CB == SM, "square tiling");
+  static_assert(NT % 32 == 0, "whole warps");
   extern __shared__ __align__(16) double A[];   // SM x (SM|1) extraction staging
   __shared__ double rs[SM];
   __shared__ double colk[2][SM];
   __shared__ double prow[2][SM];
-  __shared__ int sidx[SM], perm[SM], posof[SM], rowoff[SM + 1], rowk0[SM];
-  __shared__ int s_r, s_bad;
-  __shared__ double s_rinv;
+  __shared__ int sidx[SM], posof[SM], rowoff[SM + 1], rowk0[SM];
+  __shared__ int wperm[NW][SM];            // per-warp copies of the position->row map
+  __shared__ int s_bad;
   const int t = threadIdx.x;
   const int tr = t / TC, tc = t % TC;
   const int lane = t & 31;
+  const int warp = t >> 5;
 
   for (int bb = blockIdx.x; bb < count; bb += gridDim.x) {
     const int p = plist[bb];
@@ -345,11 +358,11 @@ __global__ void __launch_bounds__(TR * TC) factor_tile_kernel(
     for (int i = t; i < s; i += NT) {
       const int r = idx[base + i];
       sidx[i] = r;
-      perm[i] = i;
       const int a0 = ptr[r];
       rowk0[i] = a0;
       rowoff[i + 1] = ptr[r + 1] - a0;
     }
+    for (int i = lane; i < s; i += 32) wperm[warp][i] = i;
     for (int e = t; e < s * ld; e += NT) A[e] = 0.0;
     if (t == 0) s_bad = 0;
     __syncthreads();
@@ -371,6 +384,13 @@ __global__ void __launch_bounds__(TR * TC) factor_tile_kernel(
         const int i = tr + TR * ra, j = tc + TC * cb;
         a[ra][cb] = (i < s && j < s) ? A[i * ld + j] : 0.0;
       }
+    if (tc == 0) {                               // publish column 0
+#pragma unroll
+      for (int ra = 0; ra < RA; ++ra) {
+        const int i = tr + TR * ra;
+        if (i < s) colk[0][i] = a[ra][0];
+      }
+    }
     __syncthreads();
     if (s_bad) {
       if (t == 0) status[p] = s_bad;
@@ -378,94 +398,105 @@ __global__ void __launch_bounds__(TR * TC) factor_tile_kernel(
       continue;
     }
     int bad = 0;
-    for (int k = 0; k < s; ++k) {
-      const int buf = k & 1;
-      // publish pivot column k (owners: tc == k % TC)
-      if (tc == k % TC) {
-        const int kb = k / TC;
 #pragma unroll
-        for (int ra = 0; ra < RA; ++ra) {
-          const int i = tr + TR * ra;
-          double v = 0.0;
-#pragma unroll
-          for (int cb = 0; cb < CB; ++cb)
-            if (cb == kb) v = a[ra][cb];
-          if (i < s) colk[buf][i] = v;
-        }
-      }
-      __syncthreads();
-      if (t < 32) {                              // pivot search over positions k..s-1
+    for (int kb = 0; kb < CB; ++kb) {
+      for (int kt = 0; kt < TC; ++kt) {
+        const int k = kb * TC + kt;
+        if (k >= s || bad) break;
+        const int buf = k & 1;
+        // pivot search (every warp): first max |colk| over positions k..s-1
         double best = -1.0;
         int bi = s;
         for (int q = k + lane; q < s; q += 32) {
-          const double v = fabs(colk[buf][perm[q]]);
+          const double v = fabs(colk[buf][wperm[warp][q]]);
           if (v > best) {
             best = v;
             bi = q;
           }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ob > best || (ob == best && oi < bi)) {
-            best = ob;
-            bi = oi;
-          }
-        }
+        const unsigned long long key =
+            best >= 0.0 ? static_cast<unsigned long long>(__double_as_longlong(best)) : 0ull;
+        const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+        const int pos = __reduce_min_sync(
+            0xffffffffu, (hi == mhi && lo == mlo) ? bi : 0x7fffffff);
+        const int r = wperm[warp][pos];
+        const int rk = wperm[warp][k];
+        __syncwarp();
         if (lane == 0) {
-          const int tmp = perm[k];
-          perm[k] = perm[bi];
-          perm[bi] = tmp;
-          const int r = perm[k];
-          const double piv = colk[buf][r];
-          s_r = r;
-          if (!(fabs(piv) >= 1e-12 * rs[r])) {
-            s_bad = VK_PATCH_SMALL_PIVOT;
-          } else {
-            s_rinv = 1.0 / piv;
+          wperm[warp][k] = r;
+          wperm[warp][pos] = rk;
+        }
+        __syncwarp();
+        const double piv = colk[buf][r];
+        if (!(fabs(piv) >= 1e-12 * rs[r])) {     // uniform: same data in every thread
+          bad = VK_PATCH_SMALL_PIVOT;
+          break;
+        }
+        const double rinv = 1.0 / piv;
+        const bool own_row = (tr == r % TR);
+        const int rb = r / TR;
+        // scaled pivot row (owners: tr == r % TR); register block rb matched
+        // against the unrolled ra so every access is static
+        if (own_row) {
+#pragma unroll
+          for (int ra = 0; ra < RA; ++ra) {
+            if (ra == rb) {
+#pragma unroll
+              for (int cb = 0; cb < CB; ++cb) {
+                const int j = tc + TC * cb;
+                const double v = (cb == kb && tc == kt) ? rinv : a[ra][cb] * rinv;
+                if (j < s) prow[buf][j] = v;
+              }
+            }
           }
         }
-      }
-      __syncthreads();
-      if (s_bad) {
-        bad = s_bad;
-        break;
-      }
-      const int r = s_r;
-      const double rinv = s_rinv;
-      // scaled pivot row (owners: tr == r % TR)
-      if (tr == r % TR) {
-        const int rb = r / TR;
+        __syncthreads();
+        double pj[CB];
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) pj[cb] = prow[buf][tc + TC * cb];
+        // rank-1 update of the whole tile, branch-free (rows >= s are never
+        // read back; the pivot row is overwritten with its scaled copy below)
+        const bool own_k = (tc == kt);
 #pragma unroll
         for (int ra = 0; ra < RA; ++ra) {
-          if (ra != rb) continue;
+          const double f = colk[buf][tr + TR * ra];
 #pragma unroll
           for (int cb = 0; cb < CB; ++cb) {
-            const int j = tc + TC * cb;
-            const double v = (j == k) ? rinv : a[ra][cb] * rinv;
-            a[ra][cb] = v;
-            if (j < s) prow[buf][j] = v;
+            if (cb == kb) {
+              const double g = fma(-f, pj[cb], a[ra][cb]);
+              const double h = -f * rinv;
+              a[ra][cb] = own_k ? h : g;
+            } else {
+              a[ra][cb] = fma(-f, pj[cb], a[ra][cb]);
+            }
           }
         }
-      }
-      __syncthreads();
-      double pj[CB];
+        if (own_row) {
 #pragma unroll
-      for (int cb = 0; cb < CB; ++cb) {
-        const int j = tc + TC * cb;
-        pj[cb] = (j < s) ? prow[buf][j] : 0.0;
-      }
+          for (int ra = 0; ra < RA; ++ra)
+            if (ra == rb) {
 #pragma unroll
-      for (int ra = 0; ra < RA; ++ra) {
-        const int i = tr + TR * ra;
-        if (i >= s || i == r) continue;
-        const double f = colk[buf][i];
-#pragma unroll
-        for (int cb = 0; cb < CB; ++cb) {
-          const int j = tc + TC * cb;
-          a[ra][cb] = (j == k) ? -f * rinv : fma(-f, pj[cb], a[ra][cb]);
+              for (int cb = 0; cb < CB; ++cb) a[ra][cb] = pj[cb];
+            }
         }
+        // publish column k+1 (block kb, or kb+1 after the last kt)
+        if (k + 1 < s) {
+          if (kt + 1 < TC) {
+            if (tc == kt + 1) {
+#pragma unroll
+              for (int ra = 0; ra < RA; ++ra) colk[buf ^ 1][tr + TR * ra] = a[ra][kb];
+            }
+          } else if (kb + 1 < CB) {
+            if (tc == 0) {
+#pragma unroll
+              for (int ra = 0; ra < RA; ++ra)
+                colk[buf ^ 1][tr + TR * ra] = a[ra][kb + 1 < CB ? kb + 1 : kb];
+            }
+          }
+        }
+        __syncthreads();
       }
     }
     if (bad) {
@@ -473,7 +504,8 @@ __global__ void __launch_bounds__(TR * TC) factor_tile_kernel(
       __syncthreads();
       continue;
     }
-    for (int q = t; q < s; q += NT) posof[perm[q]] = q;
+    const int* perm0 = wperm[0];
+    for (int q = t; q < s; q += NT) posof[perm0[q]] = q;
     __syncthreads();
     double* dst = inv + opoff[p];
 #pragma unroll
@@ -481,7 +513,7 @@ __global__ void __launch_bounds__(TR * TC) factor_tile_kernel(
 #pragma unroll
       for (int cb = 0; cb < CB; ++cb) {
         const int pr = tr + TR * ra, pc = tc + TC * cb;
-        if (pr < s && pc < s) dst[int64_t(perm[pc]) * s + posof[pr]] = a[ra][cb];
+        if (pr < s && pc < s) dst[int64_t(perm0[pc]) * s + posof[pr]] = a[ra][cb];
       }
     if (t == 0) status[p] = VK_PATCH_OK;
     __syncthreads();
@@ -506,9 +538,9 @@ int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int
   if (!extract_only && bk.smax <= 128) {
     // register-tiled classes: (TR x TC threads, RA x CB tile per thread)
     cudaError_t e = cudaSuccess;
-#define VK_TILE(TR_, TC_, RA_, CB_)                                                              \
+#define VK_TILE(TR_, TC_, RA_, CB_, MB_)                                                         \
   do {                                                                                         \
-    auto kern = factor_tile_kernel<TR_, TC_, RA_, CB_>;                                        \
+    auto kern = factor_tile_kernel<TR_, TC_, RA_, CB_, MB_>;                                      \
     const size_t dsm = sizeof(double) * size_t(TR_ * RA_) * size_t((TR_ * RA_) | 1);          \
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));    \
     int per_sm = 1;                                                                            \
@@ -518,17 +550,19 @@ int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int
       kern<<<grid, TR_ * TC_, dsm, st>>>(d_ids, count, h->off, h->idx, a->indptr, a->indices,  \
                                          a->data, h->opoff, h->inv, d_status);                 \
   } while (0)
-    if (bk.smax <= 16) VK_TILE(8, 8, 2, 2);
-    else if (bk.smax <= 24) VK_TILE(8, 8, 3, 3);
-    else if (bk.smax <= 32) VK_TILE(8, 8, 4, 4);
-    else if (bk.smax <= 40) VK_TILE(8, 8, 5, 5);
-    else if (bk.smax <= 48) VK_TILE(8, 8, 6, 6);
-    else if (bk.smax <= 56) VK_TILE(8, 8, 7, 7);
-    else if (bk.smax <= 64) VK_TILE(8, 16, 8, 4);
-    else if (bk.smax <= 80) VK_TILE(16, 16, 5, 5);
-    else if (bk.smax <= 96) VK_TILE(16, 16, 6, 6);
-    else if (bk.smax <= 112) VK_TILE(16, 16, 7, 7);
-    else VK_TILE(16, 16, 8, 8);
+    // MB: CTAs per SM the register budget must allow (occupancy vs. spills,
+    // measured per class)
+    if (bk.smax <= 16) VK_TILE(8, 8, 2, 2, 8);
+    else if (bk.smax <= 24) VK_TILE(8, 8, 3, 3, 8);
+    else if (bk.smax <= 32) VK_TILE(8, 8, 4, 4, 8);
+    else if (bk.smax <= 40) VK_TILE(8, 8, 5, 5, 8);
+    else if (bk.smax <= 48) VK_TILE(8, 8, 6, 6, 8);
+    else if (bk.smax <= 56) VK_TILE(8, 8, 7, 7, 6);
+    else if (bk.smax <= 64) VK_TILE(8, 16, 8, 4, 4);
+    else if (bk.smax <= 80) VK_TILE(16, 16, 5, 5, 2);
+    else if (bk.smax <= 96) VK_TILE(16, 16, 6, 6, 2);
+    else if (bk.smax <= 112) VK_TILE(16, 16, 7, 7, 1);
+    else VK_TILE(16, 16, 8, 8, 1);
 #undef VK_TILE
     if (e != cudaSuccess) {
       cudaFree(d_ids);
