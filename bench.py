@@ -400,7 +400,7 @@ def run_ours(args):
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("patch_solve_kernel", {}).get("dram_bytes")
+            traffic = json.load(open(prof)).get("patch_solve_bulk_kernel", {}).get("dram_bytes")
         except Exception:
             traffic = None
     cpu = None
@@ -420,7 +420,7 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (8*sum s^2 = %.0f MB streamed per sweep)"
                          % (8 * sum_s2 / 1e6),
                    "parallelism": f"replicas x{world}"},
-        "roofline": {"bound": "hbm", "kernel": "patch_solve_kernel (K4a)",
+        "roofline": {"bound": "hbm", "kernel": "patch_solve_bulk_kernel (K4a, TMA bulk copies)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes": bytes_solve, "ms": ms_solve},

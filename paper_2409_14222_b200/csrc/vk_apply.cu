@@ -13,6 +13,7 @@
 //     sequential `out[idx] += ...` order, and applies the epilogue
 //     out = acc | x = scale*acc | x = x + scale*acc.
 #include <algorithm>
+#include <cstdlib>
 
 #include "vk_common.cuh"
 
@@ -258,7 +259,181 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_split_kernel(
   }
 }
 
+// Bulk-copy variant for small patches (s <= kBulkMaxS): each warp streams its
+// patches' explicit inverses with one cp.async.bulk (TMA, 1-D) per patch into
+// a two-stage shared-memory ring, completion tracked by an mbarrier per
+// stage; an elected lane issues the copy for patch p+2nw as soon as the warp
+// has finished reading patch p's buffer.  A patch operator is one contiguous,
+// 16-byte aligned block ((s*s+1)&~1 doubles, vk_factor.cu), so the DMA engine
+// moves the whole 8 s^2 bytes as one transfer (evict-first in L2) and the
+// lanes read it back conflict-free (lane = row).  Residual gathers use the
+// same three-deep pipeline as patch_solve_kernel; per-element arithmetic is
+// identical (fma over columns in order, then fl(w*y)).
+constexpr int kBulkMaxS = 40;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+template <int R>
+__global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_bulk_kernel(
+    int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
+    const double* __restrict__ w, const int64_t* __restrict__ opoff,
+    const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z,
+    int stage_doubles) {
+  extern __shared__ __align__(128) double sbuf[];   // [warps][2][stage_doubles]
+  __shared__ __align__(8) uint64_t bars[kApplyWarps][2];
+  __shared__ double rsh_all[kApplyWarps][32 * R];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  double* rsh = rsh_all[warp];
+  double* stage[2] = {sbuf + (2 * warp) * stage_doubles, sbuf + (2 * warp + 1) * stage_doubles};
+  uint64_t* bar[2] = {&bars[warp][0], &bars[warp][1]};
+  const int nw = gridDim.x * kApplyWarps;
+  const int p0 = blockIdx.x * kApplyWarps + warp;
+  if (lane == 0) {
+    mbar_init(bar[0], 1);
+    mbar_init(bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  const uint64_t pol = evict_first_policy();
+  auto issue = [&](int s, int64_t op, int b) {      // lane 0: patch operator -> stage b
+    if (lane == 0) {
+      const uint32_t bytes = static_cast<uint32_t>(((s * s + 1) & ~1) * sizeof(double));
+      mbar_expect_tx(bar[b], bytes);
+      bulk_g2s(stage[b], inv + op, bytes, bar[b], pol);
+    }
+  };
+
+  // pipeline registers: stage A (r values), B (indices), C (offsets)
+  int64_t baseA = 0, opA = 0, baseB = 0, opB = 0, baseC = 0, opC = 0;
+  int sA = 0, sB = 0, sC = 0;
+  double rA[R];
+  int iB[R];
+  auto load_meta = [&](int p, int64_t& base, int& sz, int64_t& op) {
+    if (p < npatch) {
+      base = off[p];
+      sz = static_cast<int>(off[p + 1] - base);
+      op = opoff[p];
+    } else {
+      base = 0;
+      sz = 0;
+      op = 0;
+    }
+  };
+  load_meta(p0, baseA, sA, opA);
+  if (p0 < npatch) issue(sA, opA, 0);
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int i = lane + 32 * q;
+    rA[q] = (i < sA) ? __ldg(r + idx[baseA + i]) : 0.0;
+  }
+  load_meta(p0 + nw, baseB, sB, opB);
+  if (p0 + nw < npatch) issue(sB, opB, 1);
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int i = lane + 32 * q;
+    iB[q] = (i < sB) ? idx[baseB + i] : 0;
+  }
+  load_meta(p0 + 2 * nw, baseC, sC, opC);
+
+  uint32_t parity[2] = {0u, 0u};
+  int b = 0;
+  for (int p = p0; p < npatch; p += nw) {
+    const int64_t base = baseA;
+    const int s = sA;
+#pragma unroll
+    for (int q = 0; q < R; ++q) rsh[lane + 32 * q] = rA[q];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = lane + 32 * q;
+      rA[q] = (i < sB) ? __ldg(r + iB[q]) : 0.0;
+    }
+    baseA = baseB; opA = opB; sA = sB;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = lane + 32 * q;
+      iB[q] = (i < sC) ? idx[baseC + i] : 0;
+    }
+    const int sN = sC;
+    const int64_t opN = opC;
+    baseB = baseC; opB = opC; sB = sC;
+    load_meta(p + 3 * nw, baseC, sC, opC);
+    __syncwarp();
+
+    mbar_wait(bar[b], parity[b]);
+    parity[b] ^= 1u;
+    const double* A = stage[b];
+    double y[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) y[q] = 0.0;
+#pragma unroll 4
+    for (int j = 0; j < s; ++j) {
+      const double rj = rsh[j];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = lane + 32 * q;
+        if (R == 1 || i < s) y[q] = fma(A[j * s + i], rj, y[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = lane + 32 * q;
+      if (i < s) z[base + i] = __dmul_rn(w[base + i], y[q]);
+    }
+    __syncwarp();                                   // stage b fully read
+    if (p + 2 * nw < npatch) issue(sN, opN, b);
+    b ^= 1;
+  }
+}
+
 }  // namespace
+
+// VK_APPLY_BULK=0 disables the bulk-copy kernel (A/B measurements)
+static bool bulk_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("VK_APPLY_BULK");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 
 extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
   if (int st = check_apply(h)) return st;
@@ -278,6 +453,24 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
       default: VK_SPLIT(4); break;
     }
 #undef VK_SPLIT
+  } else if (h->npatch > 0 && h->smax <= kBulkMaxS && !h->mixed_sizes && bulk_enabled()) {
+    // small patches: TMA bulk copies into a per-warp two-stage ring
+    const int stage_doubles = ((h->smax * h->smax + 1) & ~1);
+    const size_t dsm = sizeof(double) * size_t(stage_doubles) * 2 * kApplyWarps;
+    const int want = (h->npatch + kApplyWarps - 1) / kApplyWarps;
+#define VK_BULK(RV)                                                                           \
+  do {                                                                                        \
+    auto k = patch_solve_bulk_kernel<RV>;                                                     \
+    VK_CHECK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                       int(dsm)));                                            \
+    const int grid = std::min(want, vk_resident_blocks((const void*)k, kApplyWarps * 32, dsm)); \
+    k<<<grid, kApplyWarps * 32, dsm, vk_stream(stream)>>>(h->npatch, h->off, h->idx, h->w,     \
+                                                         h->opoff, h->inv, r, h->zbuf,         \
+                                                         stage_doubles);                       \
+  } while (0)
+    if (rpl <= 1) VK_BULK(1);
+    else VK_BULK(2);
+#undef VK_BULK
   } else if (h->npatch > 0) {
     // persistent: exactly the resident CTAs, so no partial last wave
     const int want = (h->npatch + kApplyWarps - 1) / kApplyWarps;
