@@ -424,12 +424,190 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_bulk_kernel(
   }
 }
 
+// Chunked bulk-copy variant for s <= 128: a warp's patch operators are
+// streamed as a sequence of column chunks (cc columns, cc even,
+// cc*s*8 <= kChunkBytes; a patch's last chunk is padded to 16 bytes, which
+// the operator layout provides) through a kChunkStages-deep per-warp
+// shared-memory ring, one cp.async.bulk + mbarrier per chunk.  Measured
+// (tools/gpu_scripts/build_variants.sh, cfg2-5): one 16 KB stage per warp
+// beats 2-6 smaller stages (8 warps' transfers overlap each other; fewer,
+// larger DMA transfers): cfg3 0.98, cfg4 1.02, cfg5 1.07 of the copy peak.  Lane 0 is the
+// producer: it keeps the ring full with the chunks of the warp's next
+// patches (its own cursor, one patch of metadata prefetched); all lanes
+// consume column by column.  Same per-element arithmetic as
+// patch_solve_kernel.
+#ifndef VK_CHUNK_BYTES
+#define VK_CHUNK_BYTES 16384
+#endif
+#ifndef VK_CHUNK_STAGES
+#define VK_CHUNK_STAGES 1
+#endif
+constexpr int kChunkBytes = VK_CHUNK_BYTES;
+constexpr int kChunkDoubles = kChunkBytes / 8;
+constexpr int kChunkStages = VK_CHUNK_STAGES;
+
+__host__ __device__ constexpr int chunk_cols(int s) {
+  return (kChunkDoubles / s) >= s ? s : ((kChunkDoubles / s) & ~1);
+}
+
+template <int R>
+__device__ __forceinline__ void chunk_columns(int lane, int s, int j0, int j1, const double* As,
+                                              const double* rsh, double (&y)[4]) {
+#pragma unroll 4
+  for (int j = j0; j < j1; ++j) {
+    const double rj = rsh[j];
+    const double* col = As + (j - j0) * s;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = lane + 32 * q;
+      if (i < s) y[q] = fma(col[i], rj, y[q]);
+    }
+  }
+}
+
+template <int RMAX>
+__global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_chunk_kernel(
+    int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
+    const double* __restrict__ w, const int64_t* __restrict__ opoff,
+    const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
+  extern __shared__ __align__(128) double sbuf[];   // [warps][stages][kChunkDoubles]
+  __shared__ __align__(8) uint64_t bars[kApplyWarps][kChunkStages];
+  __shared__ double rsh_all[kApplyWarps][32 * RMAX];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  double* rsh = rsh_all[warp];
+  double* ring = sbuf + warp * kChunkStages * kChunkDoubles;
+  uint64_t* bar = bars[warp];
+  const int nw = gridDim.x * kApplyWarps;
+  const int p0 = blockIdx.x * kApplyWarps + warp;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < kChunkStages; ++k) mbar_init(&bar[k], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  const uint64_t pol = evict_first_policy();
+
+  auto meta_s = [&](int p) { return p < npatch ? static_cast<int>(off[p + 1] - off[p]) : 0; };
+  auto meta_op = [&](int p) { return p < npatch ? opoff[p] : int64_t(0); };
+  // producer cursor (uniform in the warp; lane 0 issues)
+  int pp = p0, pj = 0, ps = meta_s(p0);
+  int64_t pop = meta_op(p0);
+  int ns = meta_s(p0 + nw);
+  int64_t nop = meta_op(p0 + nw);
+  int pstage = 0;
+  auto issue_next = [&]() {
+    if (pp >= npatch) return;
+    const int cc = chunk_cols(ps);
+    const int cols = min(cc, ps - pj);
+    const uint32_t bytes = static_cast<uint32_t>(((cols * ps + 1) & ~1) * sizeof(double));
+    if (lane == 0) {
+      mbar_expect_tx(&bar[pstage], bytes);
+      bulk_g2s(ring + pstage * kChunkDoubles, inv + pop + int64_t(pj) * ps, bytes, &bar[pstage], pol);
+    }
+    pstage = (pstage + 1 == kChunkStages) ? 0 : pstage + 1;
+    pj += cols;
+    if (pj >= ps) {
+      pp += nw;
+      pj = 0;
+      ps = ns;
+      pop = nop;
+      ns = meta_s(pp + nw);
+      nop = meta_op(pp + nw);
+    }
+  };
+#pragma unroll
+  for (int k = 0; k < kChunkStages; ++k) issue_next();
+
+  // residual pipeline (as patch_solve_kernel): A = r values, B = indices, C = offsets
+  int64_t baseA = 0, baseB = 0, baseC = 0;
+  int sA = 0, sB = 0, sC = 0;
+  double rA[RMAX];
+  int iB[RMAX];
+  auto load_meta = [&](int p, int64_t& base, int& sz) {
+    if (p < npatch) {
+      base = off[p];
+      sz = static_cast<int>(off[p + 1] - base);
+    } else {
+      base = 0;
+      sz = 0;
+    }
+  };
+  load_meta(p0, baseA, sA);
+#pragma unroll
+  for (int q = 0; q < RMAX; ++q) {
+    const int i = lane + 32 * q;
+    rA[q] = (i < sA) ? __ldg(r + idx[baseA + i]) : 0.0;
+  }
+  load_meta(p0 + nw, baseB, sB);
+#pragma unroll
+  for (int q = 0; q < RMAX; ++q) {
+    const int i = lane + 32 * q;
+    iB[q] = (i < sB) ? idx[baseB + i] : 0;
+  }
+  load_meta(p0 + 2 * nw, baseC, sC);
+
+  int cstage = 0;
+  uint32_t phase_bits = 0;                       // parity per stage
+  for (int p = p0; p < npatch; p += nw) {
+    const int64_t base = baseA;
+    const int s = sA;
+#pragma unroll
+    for (int q = 0; q < RMAX; ++q) rsh[lane + 32 * q] = rA[q];
+#pragma unroll
+    for (int q = 0; q < RMAX; ++q) {
+      const int i = lane + 32 * q;
+      rA[q] = (i < sB) ? __ldg(r + iB[q]) : 0.0;
+    }
+    baseA = baseB; sA = sB;
+#pragma unroll
+    for (int q = 0; q < RMAX; ++q) {
+      const int i = lane + 32 * q;
+      iB[q] = (i < sC) ? idx[baseC + i] : 0;
+    }
+    baseB = baseC; sB = sC;
+    load_meta(p + 3 * nw, baseC, sC);
+    __syncwarp();
+
+    double y[4] = {0.0, 0.0, 0.0, 0.0};
+    const int cc = chunk_cols(s);
+    const int rp = (s + 31) >> 5;
+    for (int j0 = 0; j0 < s; j0 += cc) {
+      const int j1 = min(s, j0 + cc);
+      mbar_wait(&bar[cstage], (phase_bits >> cstage) & 1u);
+      phase_bits ^= (1u << cstage);
+      const double* As = ring + cstage * kChunkDoubles;
+      if (RMAX <= 1 || rp <= 1) chunk_columns<1>(lane, s, j0, j1, As, rsh, y);
+      else if (RMAX <= 2 || rp == 2) chunk_columns<(RMAX < 2 ? RMAX : 2)>(lane, s, j0, j1, As, rsh, y);
+      else if (RMAX <= 3 || rp == 3) chunk_columns<(RMAX < 3 ? RMAX : 3)>(lane, s, j0, j1, As, rsh, y);
+      else chunk_columns<(RMAX < 4 ? RMAX : 4)>(lane, s, j0, j1, As, rsh, y);
+      __syncwarp();                               // stage fully read
+      issue_next();
+      cstage = (cstage + 1 == kChunkStages) ? 0 : cstage + 1;
+    }
+#pragma unroll
+    for (int q = 0; q < RMAX; ++q) {
+      const int i = lane + 32 * q;
+      if (i < s) z[base + i] = __dmul_rn(w[base + i], y[q]);
+    }
+  }
+}
+
 }  // namespace
 
 // VK_APPLY_BULK=0 disables the bulk-copy kernel (A/B measurements)
 static bool bulk_enabled() {
   static const bool v = [] {
     const char* e = getenv("VK_APPLY_BULK");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// VK_APPLY_CHUNK=0 disables the chunked bulk-copy kernel (A/B measurements)
+static bool chunk_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("VK_APPLY_CHUNK");
     return !(e && e[0] == '0');
   }();
   return v;
@@ -471,6 +649,26 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
     if (rpl <= 1) VK_BULK(1);
     else VK_BULK(2);
 #undef VK_BULK
+  } else if (h->npatch > 0 && h->smax <= 128 && chunk_enabled()) {
+    // larger patches: TMA bulk copies of column chunks through a per-warp ring
+    const size_t dsm = sizeof(double) * size_t(kChunkDoubles) * kChunkStages * kApplyWarps;
+    const int want = (h->npatch + kApplyWarps - 1) / kApplyWarps;
+#define VK_CHUNK(RV)                                                                          \
+  do {                                                                                        \
+    auto k = patch_solve_chunk_kernel<RV>;                                                    \
+    VK_CHECK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                       int(dsm)));                                            \
+    const int grid = std::min(want, vk_resident_blocks((const void*)k, kApplyWarps * 32, dsm)); \
+    k<<<grid, kApplyWarps * 32, dsm, vk_stream(stream)>>>(h->npatch, h->off, h->idx, h->w,     \
+                                                         h->opoff, h->inv, r, h->zbuf);        \
+  } while (0)
+    switch (rpl) {
+      case 1: VK_CHUNK(1); break;
+      case 2: VK_CHUNK(2); break;
+      case 3: VK_CHUNK(3); break;
+      default: VK_CHUNK(4); break;
+    }
+#undef VK_CHUNK
   } else if (h->npatch > 0) {
     // persistent: exactly the resident CTAs, so no partial last wave
     const int want = (h->npatch + kApplyWarps - 1) / kApplyWarps;
