@@ -145,6 +145,12 @@ VK_API int vk_patches_destroy(vk_patches_t h);
 VK_API int vk_dot(int64_t n, const double* x, const double* y, double* out_dev, void* stream);
 /* y = y - (*a_dev) * x */
 VK_API int vk_axpy_dev(int64_t n, const double* a_dev, const double* x, double* y, void* stream);
+/* Fused modified-Gram-Schmidt step (sparsela.py:160-163): y = y - (*a_dev) * x,
+ * then *out_dev = x2 . y (sqrt of it if sqrt_out; x2 may alias y).  The dot
+ * uses vk_dot's thread/element mapping and reduction tree, so the result is
+ * bit-identical to vk_axpy_dev followed by vk_dot / vk_nrm2. */
+VK_API int vk_axpy_dot(int64_t n, const double* a_dev, const double* x, double* y, const double* x2,
+                       double* out_dev, int32_t sqrt_out, void* stream);
 /* y = y + a * x  (host scalar) */
 VK_API int vk_axpy(int64_t n, double a, const double* x, double* y, void* stream);
 /* y = x / (*d_dev) */

@@ -52,6 +52,7 @@ SIGNATURES = {
     "vk_patches_destroy": (C.c_int, [_p]),
     "vk_dot": (C.c_int, [_i64, _p, _p, _p, _p]),
     "vk_axpy_dev": (C.c_int, [_i64, _p, _p, _p, _p]),
+    "vk_axpy_dot": (C.c_int, [_i64, _p, _p, _p, _p, _p, _i32, _p]),
     "vk_axpy": (C.c_int, [_i64, _f64, _p, _p, _p]),
     "vk_div_dev": (C.c_int, [_i64, _p, _p, _p, _p]),
     "vk_nrm2": (C.c_int, [_i64, _p, _p, _p]),

@@ -59,6 +59,44 @@ __global__ void __launch_bounds__(kRedBlock) dot_kernel(int64_t n, const double*
   }
 }
 
+// y -= a x, then the dot of x2 with the updated y: element i is owned by the
+// same thread as in dot_kernel (grid kRedGrid x kRedBlock, grid-stride), so
+// the per-thread fma order and the reduction are those of dot_kernel.
+template <int FIN>
+__global__ void __launch_bounds__(kRedBlock) axpy_dot_kernel(int64_t n, const double* __restrict__ a,
+                                                             const double* __restrict__ x,
+                                                             double* y, const double* x2,
+                                                             double* __restrict__ out) {
+  __shared__ double sh[kRedBlock];
+  __shared__ bool last;
+  const double av = *a;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(kRedBlock) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * kRedBlock) {
+    const double yn = __dsub_rn(y[i], __dmul_rn(av, x[i]));
+    y[i] = yn;
+    acc = fma(x2 == y ? yn : x2[i], yn, acc);
+  }
+  const double bs = block_sum(acc, sh);
+  if (threadIdx.x == 0) {
+    g_partials[blockIdx.x] = bs;
+    __threadfence();
+    const unsigned int ticket = atomicAdd(&g_arrive, 1u);
+    last = (ticket == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double v = 0.0;
+    for (int b = threadIdx.x; b < gridDim.x; b += kRedBlock) v = __dadd_rn(v, *((volatile double*)&g_partials[b]));
+    const double tot = block_sum(v, sh);
+    if (threadIdx.x == 0) {
+      *out = FIN ? sqrt(tot) : tot;
+      g_arrive = 0;
+    }
+  }
+}
+
 __global__ void axpy_dev_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ x,
                                 double* __restrict__ y) {
   const double av = *a;
@@ -134,23 +172,34 @@ __global__ void project_apply_kernel(int64_t n, const double* __restrict__ q, co
 #define VK_VEC_GRID(n) vk_grid((n), 256, 148 * 8)
 
 extern "C" int vk_dot(int64_t n, const double* x, const double* y, double* out_dev, void* stream) {
-  VK_REQUIRE(x && y && out_dev && n >= 0, "vk_dot: bad argument");
+  VK_REQUIRE(out_dev && n >= 0 && (n == 0 || (x && y)), "vk_dot: bad argument");
   dot_kernel<0><<<kRedGrid, kRedBlock, 0, vk_stream(stream)>>>(n, x, y, out_dev);
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
 
 extern "C" int vk_nrm2(int64_t n, const double* x, double* out_dev, void* stream) {
-  VK_REQUIRE(x && out_dev && n >= 0, "vk_nrm2: bad argument");
+  VK_REQUIRE(out_dev && n >= 0 && (n == 0 || x), "vk_nrm2: bad argument");
   dot_kernel<1><<<kRedGrid, kRedBlock, 0, vk_stream(stream)>>>(n, x, x, out_dev);
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
 
 extern "C" int vk_axpy_dev(int64_t n, const double* a_dev, const double* x, double* y, void* stream) {
-  VK_REQUIRE(a_dev && x && y, "vk_axpy_dev: null argument");
+  VK_REQUIRE(a_dev && (n == 0 || (x && y)), "vk_axpy_dev: null argument");
   if (n == 0) return VK_OK;
   axpy_dev_kernel<<<VK_VEC_GRID(n), 256, 0, vk_stream(stream)>>>(n, a_dev, x, y);
+  VK_CHECK_LAUNCH();
+  return VK_OK;
+}
+
+extern "C" int vk_axpy_dot(int64_t n, const double* a_dev, const double* x, double* y, const double* x2,
+                           double* out_dev, int32_t sqrt_out, void* stream) {
+  VK_REQUIRE(a_dev && out_dev && n >= 0 && (n == 0 || (x && y && x2)), "vk_axpy_dot: bad argument");
+  if (sqrt_out)
+    axpy_dot_kernel<1><<<kRedGrid, kRedBlock, 0, vk_stream(stream)>>>(n, a_dev, x, y, x2, out_dev);
+  else
+    axpy_dot_kernel<0><<<kRedGrid, kRedBlock, 0, vk_stream(stream)>>>(n, a_dev, x, y, x2, out_dev);
   VK_CHECK_LAUNCH();
   return VK_OK;
 }

@@ -425,10 +425,17 @@ def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
         w.copy_(wz)
         proj(w)
         L.call("vk_nrm2", n, L.ptr(w), L.ptr(scal[max_it + 1:]), s_)      # wnorm0
-        for i in range(j + 1):                                            # MGS (sparsela.py:160-163)
-            L.call("vk_dot", n, L.ptr(vmat[i]), L.ptr(w), L.ptr(scal[i:]), s_)
-            L.call("vk_axpy_dev", n, L.ptr(scal[i:]), L.ptr(vmat[i]), L.ptr(w), s_)
-        L.call("vk_nrm2", n, L.ptr(w), L.ptr(scal[j + 1:]), s_)
+        # MGS (sparsela.py:160-163): h_0 = v_0.w, then for each i the update
+        # w -= h_i v_i fused with the next dot (v_{i+1}.w, or ||w|| after the
+        # last one) -- bit-identical to separate dot / axpy / nrm2 kernels
+        L.call("vk_dot", n, L.ptr(vmat[0]), L.ptr(w), L.ptr(scal[0:]), s_)
+        for i in range(j + 1):
+            if i < j:
+                L.call("vk_axpy_dot", n, L.ptr(scal[i:]), L.ptr(vmat[i]), L.ptr(w),
+                       L.ptr(vmat[i + 1]), L.ptr(scal[i + 1:]), 0, s_)
+            else:
+                L.call("vk_axpy_dot", n, L.ptr(scal[i:]), L.ptr(vmat[i]), L.ptr(w),
+                       L.ptr(w), L.ptr(scal[j + 1:]), 1, s_)
         L.call("vk_div_dev", n, L.ptr(w), L.ptr(scal[j + 1:]), L.ptr(vmat[j + 1]), s_)
 
     converged = False

@@ -159,3 +159,30 @@ def test_apply_accumulation_order_matches_reference(V):
     for p in patches:
         ref[p.indices] += p.weights * (inv[p.indices] * r[p.indices])
     assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("n", [0, 1, 257, 75_776, 592_387])
+def test_fused_mgs_step_bit_identical(V, n):
+    """vk_axpy_dot == vk_axpy_dev then vk_dot / vk_nrm2, bit for bit."""
+    import torch
+    from paper_2409_14222_b200 import _lib as L
+    rng = np.random.default_rng(n)
+    x = torch.from_numpy(rng.standard_normal(n)).cuda()
+    x2 = torch.from_numpy(rng.standard_normal(n)).cuda()
+    w0 = torch.from_numpy(rng.standard_normal(n)).cuda()
+    a = torch.tensor([0.37], dtype=torch.float64, device="cuda")
+    st = L.stream_ptr()
+    for sqrt_out in (0, 1):
+        w1, w2 = w0.clone(), w0.clone()
+        o1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        o2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        L.call("vk_axpy_dev", n, L.ptr(a), L.ptr(x), L.ptr(w1), st)
+        if sqrt_out:
+            L.call("vk_nrm2", n, L.ptr(w1), L.ptr(o1), st)
+            L.call("vk_axpy_dot", n, L.ptr(a), L.ptr(x), L.ptr(w2), L.ptr(w2), L.ptr(o2), 1, st)
+        else:
+            L.call("vk_dot", n, L.ptr(x2), L.ptr(w1), L.ptr(o1), st)
+            L.call("vk_axpy_dot", n, L.ptr(a), L.ptr(x), L.ptr(w2), L.ptr(x2), L.ptr(o2), 0, st)
+        torch.cuda.synchronize()
+        assert torch.equal(w1, w2)
+        assert o1.cpu().numpy().view(np.uint64)[0] == o2.cpu().numpy().view(np.uint64)[0]
