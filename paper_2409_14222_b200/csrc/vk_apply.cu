@@ -270,6 +270,8 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_split_kernel(
 // same three-deep pipeline as patch_solve_kernel; per-element arithmetic is
 // identical (fma over columns in order, then fl(w*y)).
 constexpr int kBulkMaxS = 40;
+constexpr size_t kBulkMaxSmem =
+    sizeof(double) * size_t((kBulkMaxS * kBulkMaxS + 1) & ~1) * 2 * kApplyWarps;
 
 template <int R>
 __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_bulk_kernel(
@@ -599,8 +601,9 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
 #define VK_BULK(RV)                                                                           \
   do {                                                                                        \
     auto k = patch_solve_bulk_kernel<RV>;                                                     \
-    VK_CHECK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                                       int(dsm)));                                            \
+    static const cudaError_t attr = cudaFuncSetAttribute(                                     \
+        k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBulkMaxSmem));                   \
+    VK_CHECK_CUDA(attr);                                                                      \
     const int grid = std::min(want, vk_resident_blocks((const void*)k, kApplyWarps * 32, dsm)); \
     k<<<grid, kApplyWarps * 32, dsm, vk_stream(stream)>>>(h->npatch, h->off, h->idx, h->w,     \
                                                          h->opoff, h->inv, r, h->zbuf,         \
@@ -616,8 +619,9 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
 #define VK_CHUNK(RV)                                                                          \
   do {                                                                                        \
     auto k = patch_solve_chunk_kernel<RV>;                                                    \
-    VK_CHECK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                                       int(dsm)));                                            \
+    static const cudaError_t attr = cudaFuncSetAttribute(                                     \
+        k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));                            \
+    VK_CHECK_CUDA(attr);                                                                      \
     const int grid = std::min(want, vk_resident_blocks((const void*)k, kApplyWarps * 32, dsm)); \
     k<<<grid, kApplyWarps * 32, dsm, vk_stream(stream)>>>(h->npatch, h->off, h->idx, h->w,     \
                                                          h->opoff, h->inv, r, h->zbuf);        \

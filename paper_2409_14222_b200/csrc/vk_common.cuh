@@ -4,8 +4,9 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <map>
 #include <mutex>
-#include <unordered_map>
+#include <tuple>
 #include <vector>
 
 #include "../../include/vanka_b200.h"
@@ -108,13 +109,15 @@ static inline int vk_grid(int64_t work, int block, int cap = 148 * 16) {
 }
 
 // Blocks of `kernel` that are resident on the whole device at once (SM count
-// x occupancy), cached per kernel.  Persistent grid-stride kernels launch
-// exactly this many so there is no partial last wave.
+// x occupancy), cached per (kernel, block size, dynamic shared memory).
+// Persistent grid-stride kernels launch exactly this many so there is no
+// partial last wave.
 static inline int vk_resident_blocks(const void* kernel, int block, size_t smem = 0) {
   static std::mutex mu;
-  static std::unordered_map<const void*, int> cache;
+  static std::map<std::tuple<const void*, int, size_t>, int> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto it = cache.find(kernel);
+  const auto key = std::make_tuple(kernel, block, smem);
+  auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
@@ -123,7 +126,7 @@ static inline int vk_resident_blocks(const void* kernel, int block, size_t smem 
       per_sm < 1)
     per_sm = 1;
   const int n = per_sm * sms;
-  cache.emplace(kernel, n);
+  cache.emplace(key, n);
   return n;
 }
 
