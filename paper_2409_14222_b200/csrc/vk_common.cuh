@@ -23,10 +23,11 @@ struct Csr {
   int32_t* indices = nullptr;
   double* data = nullptr;
   double mean_row = 0.0;
+  double warp_max_mean = 0.0;  // mean over 32-row groups of the longest row
   int32_t max_row = 0;
   // CSR-stream schedule: row blocks of <= kStreamNnz nonzeros / kStreamRows rows
   int32_t nblocks = 0;
-  int32_t* rowblk = nullptr;   // [nblocks+1]
+  int2* blk = nullptr;         // [nblocks+1] (first row, first nonzero) of each block
 };
 
 #ifndef VK_STREAM_THREADS
@@ -64,6 +65,11 @@ struct Patches {
   bool factored = false;
   // host copies of the schedule (sizes) for bucketing
   std::vector<int64_t> h_off;
+  // factor schedule, built by the first factorization (sizes never change):
+  // patch ids grouped by size class, and (smax, first, count) per class
+  int32_t* fac_ids = nullptr;
+  int32_t* fac_status = nullptr;  // [npatch]
+  std::vector<std::tuple<int, int, int>> fac_classes;
 };
 
 }  // namespace vk

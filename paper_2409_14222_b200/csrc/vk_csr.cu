@@ -21,6 +21,19 @@
 
 #include "vk_common.cuh"
 
+#ifndef VK_CSR_SKEW
+#define VK_CSR_SKEW 1
+#endif
+#ifndef VK_CSR_PRE  // (experiment) stage b / y rows in shared memory by cp.async
+#define VK_CSR_PRE 0
+#endif
+#ifndef VK_CSR_SHORT  // thread-per-row kernel when the mean over 32-row groups of
+#define VK_CSR_SHORT 11  // the longest row is <= this (measured: transfers P of cfg2/3)
+#endif
+#ifndef VK_CSR_CARVE  // (experiment) force the max-shared carveout
+#define VK_CSR_CARVE 0
+#endif
+
 namespace vk {
 
 static thread_local char g_err[1024] = "";
@@ -48,22 +61,54 @@ using vk::kStreamRows;
 using vk::kStreamThreads;
 using vk::kStreamU;
 
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+}
+#if VK_CSR_PRE
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+#endif
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 // MODE 0: y = alpha*Ax + beta*y (beta == 0: y not read);  MODE 1: y = b - A x
+//
+// Latency chain per CTA (what bounds the one-wave transfers): the block table
+// holds (first row, first nonzero) pairs, so the (col, val) loads of the first
+// chunk, the row-pointer loads and the epilogue operand (b or y) are all in
+// flight together; only the x gathers wait for col.
 template <int MODE>
 __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
-    const int* __restrict__ rowblk, const int* __restrict__ ptr, const int* __restrict__ col,
+    const int2* __restrict__ blk, const int* __restrict__ ptr, const int* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
     double alpha, double beta, const double* __restrict__ b) {
   __shared__ double prod[kStreamNnz];
   __shared__ int sptr[kStreamRows + 1];
+#if VK_CSR_PRE
+  __shared__ double spre[kStreamRows];
+#endif
   __shared__ double carry;
   const int t = threadIdx.x;
-  const int r0 = rowblk[blockIdx.x], r1 = rowblk[blockIdx.x + 1];
-  const int nr = r1 - r0;
-  for (int i = t; i <= nr; i += kStreamThreads) sptr[i] = ptr[r0 + i];
-  __syncthreads();
-  const int k0 = sptr[0], k1 = sptr[nr];
+  const int2 e0 = blk[blockIdx.x], e1 = blk[blockIdx.x + 1];
+  const int r0 = e0.x, k0 = e0.y, k1 = e1.y;
+  const int nr = e1.x - r0;
   const bool single = (nr == 1);
+  // epilogue operand (b or y) of every row, staged by cp.async (no registers
+  // held across the chunk loads)
+#if VK_CSR_PRE
+  if (MODE == 1 || beta != 0.0) {
+    const double* src = (MODE == 1) ? b : y;
+    for (int i = t; i < nr; i += kStreamThreads) cp_async8(spre + i, src + r0 + i);
+  }
+#define VK_PRE(i) spre[i]
+#else
+#define VK_PRE(i) ((MODE == 1) ? b[r0 + (i)] : y[r0 + (i)])
+#endif
+  for (int i = t; i <= nr; i += kStreamThreads) cp_async4(sptr + i, ptr + r0 + i);
   if (t == 0) carry = 0.0;
   for (int kc = k0; kc < k1 || (kc == k0 && k0 == k1); kc += kStreamNnz) {
     const int kend = min(k1, kc + kStreamNnz);
@@ -80,6 +125,7 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
       const int k = kc + t + u * kStreamThreads;
       if (k < kend) prod[k - kc] = __dmul_rn(v[u], __ldg(x + c[u]));
     }
+    cp_async_wait_all();
     __syncthreads();
     if (single) {
       // a row longer than one chunk: thread 0 carries the sequential sum
@@ -89,32 +135,43 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
         carry = s;
       }
     } else {
-      // One thread per row.  Lane l starts d = (a - l) mod 16 steps late, so
-      // at every step the half-warp reads 16 distinct 8-byte bank slots
-      // ((a + k) mod 16 == (step + l) mod 16) instead of colliding whenever
-      // row starts agree mod 16; each row is still summed left to right.
+      // One thread per row, each row summed left to right.  Rows whose
+      // starts fall in the same 8-byte bank slot (within a half-warp) would
+      // serialise every shared-memory step; lane l therefore starts d steps
+      // late, d = its rank among the half-warp lanes sharing its start slot,
+      // which spreads a g-way collision over g consecutive slots at a cost of
+      // g - 1 extra steps (0 for conflict-free starts such as short rows).
       for (int i0 = 0; i0 < nr; i0 += kStreamThreads) {
         const int i = i0 + t;
-        int a = 0, len = 0, d = 0;
+        const int lane = t & 31;
+        int a = 0, len = 0;
         if (i < nr) {
           a = sptr[i] - kc;
           len = sptr[i + 1] - kc - a;
-          d = (a - (t & 31)) & 15;
         }
+#if VK_CSR_SKEW == 1  // (experiment) full skew: every lane d = (a - l) mod 16
+        const int d = len > 0 ? (a - lane) & 15 : 0;
+#elif VK_CSR_SKEW == 0  // (experiment) no skew
+        const int d = 0;
+#else
+        const int key = len > 0 ? ((a & 15) | (lane & 16)) : 32 + lane;
+        const unsigned same = __match_any_sync(0xffffffffu, key);
+        const int d = __popc(same & ((1u << lane) - 1u));
+#endif
         const int steps = __reduce_max_sync(0xffffffffu, len > 0 ? len + d : 0);
         double s = 0.0;
 #pragma unroll 4
-        for (int q = 0; q < steps; ++q) {
-          const int k = q - d;
+        for (int st = 0; st < steps; ++st) {
+          const int k = st - d;
           if (k >= 0 && k < len) s = __dadd_rn(s, prod[a + k]);
         }
         if (i >= nr) continue;
         const int row = r0 + i;
         if (MODE == 1) {
-          y[row] = __dsub_rn(b[row], s);
+          y[row] = __dsub_rn(VK_PRE(i), s);
         } else {
           double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
-          if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[row] : __dmul_rn(beta, y[row]), out);
+          if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? VK_PRE(i) : __dmul_rn(beta, VK_PRE(i)), out);
           y[row] = out;
         }
       }
@@ -125,12 +182,51 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
   if (single && t == 0) {
     const double s = carry;
     if (MODE == 1) {
-      y[r0] = __dsub_rn(b[r0], s);
+      y[r0] = __dsub_rn(VK_PRE(0), s);
     } else {
       double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
-      if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[r0] : __dmul_rn(beta, y[r0]), out);
+      if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? VK_PRE(0) : __dmul_rn(beta, VK_PRE(0)), out);
       y[r0] = out;
     }
+  }
+}
+
+// Short-row kernel (thread per row): for matrices with a few nonzeros per
+// row (prolongations) the shared-memory staging of the stream kernel costs
+// more than it saves.  Same per-row operation order (sequential, FMA-free).
+template <int MODE>
+__global__ void __launch_bounds__(256) csr_row_kernel(
+    int nrows, const int* __restrict__ ptr, const int* __restrict__ col,
+    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+    double alpha, double beta, const double* __restrict__ b) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nrows) return;
+  const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+  double pre = 0.0;
+  if (MODE == 1) pre = __ldg(b + row);
+  else if (beta != 0.0) pre = y[row];
+  double s = 0.0;
+  int k = k0;
+  for (; k + 4 <= k1; k += 4) {
+    int c[4];
+    double v[4], p[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      c[u] = __ldg(col + k + u);
+      v[u] = __ldg(val + k + u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) p[u] = __dmul_rn(v[u], __ldg(x + c[u]));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s = __dadd_rn(s, p[u]);
+  }
+  for (; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(__ldg(val + k), __ldg(x + __ldg(col + k))));
+  if (MODE == 1) {
+    y[row] = __dsub_rn(pre, s);
+  } else {
+    double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
+    if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? pre : __dmul_rn(beta, pre), out);
+    y[row] = out;
   }
 }
 
@@ -138,7 +234,18 @@ template <int MODE>
 cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alpha, double beta,
                         const double* b, cudaStream_t st) {
   if (a.nblocks == 0) return cudaSuccess;
-  csr_stream_kernel<MODE><<<a.nblocks, kStreamThreads, 0, st>>>(a.rowblk, a.indptr, a.indices,
+  if (a.warp_max_mean <= VK_CSR_SHORT) {
+    csr_row_kernel<MODE><<<(a.nrows + 255) / 256, 256, 0, st>>>(a.nrows, a.indptr, a.indices,
+                                                               a.data, x, y, alpha, beta, b);
+    return cudaGetLastError();
+  }
+#if VK_CSR_CARVE
+  static const cudaError_t carve = cudaFuncSetAttribute(
+      csr_stream_kernel<MODE>, cudaFuncAttributePreferredSharedMemoryCarveout,
+      cudaSharedmemCarveoutMaxShared);
+  if (carve != cudaSuccess) return carve;
+#endif
+  csr_stream_kernel<MODE><<<a.nblocks, kStreamThreads, 0, st>>>(a.blk, a.indptr, a.indices,
                                                                a.data, x, y, alpha, beta, b);
   return cudaGetLastError();
 }
@@ -199,10 +306,12 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
   e = cudaMalloc(&a->indptr, sizeof(int32_t) * (nrows + 1));
   if (e == cudaSuccess) e = cudaMalloc(&a->indices, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
   if (e == cudaSuccess) e = cudaMalloc(&a->data, sizeof(double) * std::max<int64_t>(nnz, 1));
-  if (e == cudaSuccess) e = cudaMalloc(&a->rowblk, sizeof(int32_t) * rb.size());
+  std::vector<int2> bt(rb.size());
+  for (size_t i = 0; i < rb.size(); ++i) bt[i] = make_int2(rb[i], hp[rb[i]]);
+  if (e == cudaSuccess) e = cudaMalloc(&a->blk, sizeof(int2) * bt.size());
   if (e == cudaSuccess)
     e = cudaMemcpy(a->indptr, hp.data(), sizeof(int32_t) * (nrows + 1), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(a->rowblk, rb.data(), sizeof(int32_t) * rb.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(a->blk, bt.data(), sizeof(int2) * bt.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && nnz)
     e = cudaMemcpy(a->indices, indices, sizeof(int32_t) * nnz, cudaMemcpyDefault);
   if (e == cudaSuccess && nnz) e = cudaMemcpy(a->data, data, sizeof(double) * nnz, cudaMemcpyDefault);
@@ -211,7 +320,7 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
     cudaFree(a->indptr);
     cudaFree(a->indices);
     cudaFree(a->data);
-    cudaFree(a->rowblk);
+    cudaFree(a->blk);
     delete a;
     return VK_ERR_CUDA;
   }
@@ -219,6 +328,16 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
   for (int32_t i = 0; i < nrows; ++i) mx = std::max(mx, hp[i + 1] - hp[i]);
   a->max_row = mx;
   a->mean_row = nrows ? double(nnz) / nrows : 0.0;
+  // divergence measure of a thread-per-row schedule: mean over 32-row groups
+  // of the longest row in the group
+  double wsum = 0.0;
+  int32_t ng = 0;
+  for (int32_t g = 0; g < nrows; g += 32, ++ng) {
+    int32_t m = 0;
+    for (int32_t i = g; i < std::min(nrows, g + 32); ++i) m = std::max(m, hp[i + 1] - hp[i]);
+    wsum += m;
+  }
+  a->warp_max_mean = ng ? wsum / ng : 0.0;
   *out = a;
   return VK_OK;
 }
@@ -263,7 +382,7 @@ extern "C" int vk_csr_destroy(vk_csr_t a) {
   cudaFree(a->indptr);
   cudaFree(a->indices);
   cudaFree(a->data);
-  cudaFree(a->rowblk);
+  cudaFree(a->blk);
   delete a;
   return VK_OK;
 }

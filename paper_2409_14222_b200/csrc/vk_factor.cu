@@ -21,6 +21,7 @@
 // register-tiled kernel (factor_tile_kernel), larger ones the shared-memory
 // kernel (factor_kernel, also used for the extraction-only export).
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -520,22 +521,13 @@ __global__ void __launch_bounds__(TR * TC, MB) factor_tile_kernel(
   }
 }
 
-int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int* d_status,
-                  double* blocks, const std::vector<int64_t>* blk_off_host, int extract_only,
-                  cudaStream_t st) {
-  if (bk.ids.empty()) return VK_OK;
-  int* d_ids = nullptr;
-  int64_t* d_boff = nullptr;
-  VK_CHECK_CUDA(cudaMalloc(&d_ids, sizeof(int) * bk.ids.size()));
-  VK_CHECK_CUDA(cudaMemcpy(d_ids, bk.ids.data(), sizeof(int) * bk.ids.size(), cudaMemcpyHostToDevice));
-  if (blk_off_host) {
-    VK_CHECK_CUDA(cudaMalloc(&d_boff, sizeof(int64_t) * blk_off_host->size()));
-    VK_CHECK_CUDA(cudaMemcpy(d_boff, blk_off_host->data(), sizeof(int64_t) * blk_off_host->size(),
-                             cudaMemcpyHostToDevice));
-  }
-  const size_t smem = factor_smem_bytes(bk.smax);
-  const int count = static_cast<int>(bk.ids.size());
-  if (!extract_only && bk.smax <= 128) {
+// One size class: d_ids (device) lists its patches.  Asynchronous on st.
+int launch_class(int smax, const int* d_ids, int count, const vk_patches_s* h, const vk::Csr* a,
+                 int* d_status, double* blocks, const int64_t* d_boff, int extract_only,
+                 cudaStream_t st) {
+  if (count == 0) return VK_OK;
+  const size_t smem = factor_smem_bytes(smax);
+  if (!extract_only && smax <= 128) {
     // register-tiled classes: (TR x TC threads, RA x CB tile per thread)
     cudaError_t e = cudaSuccess;
 #define VK_TILE(TR_, TC_, RA_, CB_, MB_)                                                         \
@@ -552,30 +544,29 @@ int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int
   } while (0)
     // MB: CTAs per SM the register budget must allow (occupancy vs. spills,
     // measured per class)
-    if (bk.smax <= 16) VK_TILE(8, 8, 2, 2, 8);
-    else if (bk.smax <= 24) VK_TILE(8, 8, 3, 3, 8);
-    else if (bk.smax <= 32) VK_TILE(8, 8, 4, 4, 8);
-    else if (bk.smax <= 40) VK_TILE(8, 8, 5, 5, 8);
-    else if (bk.smax <= 48) VK_TILE(8, 8, 6, 6, 8);
-    else if (bk.smax <= 56) VK_TILE(8, 8, 7, 7, 6);
-    else if (bk.smax <= 64) VK_TILE(8, 16, 8, 4, 4);
-    else if (bk.smax <= 80) VK_TILE(16, 16, 5, 5, 2);
-    else if (bk.smax <= 96) VK_TILE(16, 16, 6, 6, 2);
-    else if (bk.smax <= 112) VK_TILE(16, 16, 7, 7, 1);
+    if (smax <= 16) VK_TILE(8, 8, 2, 2, 8);
+    else if (smax <= 24) VK_TILE(8, 8, 3, 3, 8);
+    else if (smax <= 32) VK_TILE(8, 8, 4, 4, 8);
+    else if (smax <= 40) VK_TILE(8, 8, 5, 5, 8);
+    else if (smax <= 48) VK_TILE(8, 8, 6, 6, 8);
+    else if (smax <= 56) VK_TILE(8, 8, 7, 7, 6);
+    else if (smax <= 64) VK_TILE(8, 16, 8, 4, 4);
+    else if (smax <= 80) VK_TILE(16, 16, 5, 5, 2);
+    else if (smax <= 96) VK_TILE(16, 16, 6, 6, 2);
+    else if (smax <= 112) VK_TILE(16, 16, 7, 7, 1);
     else VK_TILE(16, 16, 8, 8, 1);
 #undef VK_TILE
     if (e != cudaSuccess) {
-      cudaFree(d_ids);
       vk::set_error("factor_tile_kernel: %s", cudaGetErrorString(e));
       return VK_ERR_CUDA;
     }
-  } else if (bk.smax <= 32) {
+  } else if (smax <= 32) {
     VK_CHECK_CUDA(cudaFuncSetAttribute(factor_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(smem)));
     factor_kernel<128><<<std::min(count, 148 * 32), 128, smem, st>>>(
         d_ids, count, h->off, h->idx, a->indptr, a->indices, a->data, h->opoff, h->inv, d_status,
         blocks, d_boff, extract_only);
-  } else if (bk.smax <= 64) {
+  } else if (smax <= 64) {
     VK_CHECK_CUDA(cudaFuncSetAttribute(factor_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(smem)));
     factor_kernel<256><<<std::min(count, 148 * 16), 256, smem, st>>>(
@@ -588,14 +579,35 @@ int launch_bucket(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int
         d_ids, count, h->off, h->idx, a->indptr, a->indices, a->data, h->opoff, h->inv, d_status,
         blocks, d_boff, extract_only);
   }
-  cudaError_t e = cudaStreamSynchronize(st);
-  cudaFree(d_ids);
-  cudaFree(d_boff);
+  const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     vk::set_error("factor_kernel: %s", cudaGetErrorString(e));
     return VK_ERR_CUDA;
   }
   return VK_OK;
+}
+
+// extraction-only export path: upload the class lists, launch, wait
+int launch_bucket_sync(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a, int* d_status,
+                       double* blocks, const std::vector<int64_t>& blk_off_host) {
+  if (bk.ids.empty()) return VK_OK;
+  int* d_ids = nullptr;
+  int64_t* d_boff = nullptr;
+  VK_CHECK_CUDA(cudaMalloc(&d_ids, sizeof(int) * bk.ids.size()));
+  VK_CHECK_CUDA(cudaMalloc(&d_boff, sizeof(int64_t) * blk_off_host.size()));
+  VK_CHECK_CUDA(cudaMemcpy(d_ids, bk.ids.data(), sizeof(int) * bk.ids.size(), cudaMemcpyHostToDevice));
+  VK_CHECK_CUDA(cudaMemcpy(d_boff, blk_off_host.data(), sizeof(int64_t) * blk_off_host.size(),
+                           cudaMemcpyHostToDevice));
+  int st = launch_class(bk.smax, d_ids, static_cast<int>(bk.ids.size()), h, a, d_status, blocks,
+                        d_boff, 1, 0);
+  const cudaError_t e = cudaDeviceSynchronize();
+  cudaFree(d_ids);
+  cudaFree(d_boff);
+  if (!st && e != cudaSuccess) {
+    vk::set_error("factor_kernel: %s", cudaGetErrorString(e));
+    st = VK_ERR_CUDA;
+  }
+  return st;
 }
 
 }  // namespace
@@ -633,7 +645,7 @@ extern "C" int vk_patches_extract(vk_patches_t h, vk_csr_t a, int32_t first, int
   for (auto& bk : buckets) {
     std::vector<int64_t> boff(bk.ids.size());
     for (size_t q = 0; q < bk.ids.size(); ++q) boff[q] = rel[bk.ids[q] - first];
-    st = launch_bucket(bk, h, a, d_status, d_blocks, &boff, 1, 0);
+    st = launch_bucket_sync(bk, h, a, d_status, d_blocks, boff);
     if (st) break;
   }
   if (!st) {
@@ -657,53 +669,88 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
                   kMaxPatch);
     return VK_ERR_UNSUPPORTED;
   }
-  // operator storage: s^2 rounded to even (16-byte aligned per patch)
-  std::vector<int64_t> oo(h->npatch + 1, 0);
-  for (int p = 0; p < h->npatch; ++p) {
-    const int64_t s = h->h_off[p + 1] - h->h_off[p];
-    oo[p + 1] = oo[p] + ((s * s + 1) & ~int64_t(1));
+  if (!h->fac_status) {
+    // first factorization: operator storage (s^2 rounded to even, 16-byte
+    // aligned per patch) and the size-class schedule, kept in the handle
+    std::vector<int64_t> oo(h->npatch + 1, 0);
+    for (int p = 0; p < h->npatch; ++p) {
+      const int64_t s = h->h_off[p + 1] - h->h_off[p];
+      oo[p + 1] = oo[p] + ((s * s + 1) & ~int64_t(1));
+    }
+    if (!h->opoff) VK_CHECK_CUDA(cudaMalloc(&h->opoff, sizeof(int64_t) * (h->npatch + 1)));
+    VK_CHECK_CUDA(cudaMemcpy(h->opoff, oo.data(), sizeof(int64_t) * (h->npatch + 1), cudaMemcpyHostToDevice));
+    if (h->inv && h->inv_total != oo[h->npatch]) {
+      cudaFree(h->inv);
+      h->inv = nullptr;
+    }
+    if (!h->inv) {
+      VK_CHECK_CUDA(cudaMalloc(&h->inv, sizeof(double) * std::max<int64_t>(oo[h->npatch], 2)));
+      h->inv_total = oo[h->npatch];
+    }
+    auto buckets = make_buckets(h->h_off, 0, h->npatch);
+    std::vector<int32_t> ids;
+    std::vector<std::pair<double, std::tuple<int, int, int>>> cls;
+    for (auto& bk : buckets) {
+      if (bk.ids.empty()) continue;
+      double work = 0.0;
+      for (int q : bk.ids) work += std::pow(double(h->h_off[q + 1] - h->h_off[q]), 3);
+      cls.push_back({work, {bk.smax, int(ids.size()), int(bk.ids.size())}});
+      ids.insert(ids.end(), bk.ids.begin(), bk.ids.end());
+    }
+    std::sort(cls.begin(), cls.end(), [](auto& x, auto& y) { return x.first > y.first; });
+    h->fac_classes.clear();
+    for (auto& c : cls) h->fac_classes.push_back(c.second);
+    VK_CHECK_CUDA(cudaMalloc(&h->fac_ids, sizeof(int32_t) * std::max<size_t>(ids.size(), 1)));
+    if (!ids.empty())
+      VK_CHECK_CUDA(cudaMemcpy(h->fac_ids, ids.data(), sizeof(int32_t) * ids.size(), cudaMemcpyHostToDevice));
+    VK_CHECK_CUDA(cudaMalloc(&h->fac_status, sizeof(int32_t) * std::max(h->npatch, 1)));
   }
-  if (!h->opoff) VK_CHECK_CUDA(cudaMalloc(&h->opoff, sizeof(int64_t) * (h->npatch + 1)));
-  VK_CHECK_CUDA(cudaMemcpy(h->opoff, oo.data(), sizeof(int64_t) * (h->npatch + 1), cudaMemcpyHostToDevice));
-  if (h->inv && h->inv_total != oo[h->npatch]) {
-    cudaFree(h->inv);
-    h->inv = nullptr;
+  int* d_status = h->fac_status;
+  // The largest class (most work) runs on the legacy stream, the small ones
+  // (boundary / coarse patches) beside it on an auxiliary stream; one join.
+  static cudaStream_t aux = nullptr;
+  static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (!aux) {
+    VK_CHECK_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    VK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    VK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
   }
-  if (!h->inv) {
-    VK_CHECK_CUDA(cudaMalloc(&h->inv, sizeof(double) * std::max<int64_t>(oo[h->npatch], 2)));
-    h->inv_total = oo[h->npatch];
-  }
-  int* d_status = nullptr;
-  VK_CHECK_CUDA(cudaMalloc(&d_status, sizeof(int) * std::max(h->npatch, 1)));
-  VK_CHECK_CUDA(cudaMemset(d_status, 0, sizeof(int) * std::max(h->npatch, 1)));
-  auto buckets = make_buckets(h->h_off, 0, h->npatch);
+  VK_CHECK_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int) * std::max(h->npatch, 1), 0));
+  VK_CHECK_CUDA(cudaEventRecord(ev_fork, 0));
+  VK_CHECK_CUDA(cudaStreamWaitEvent(aux, ev_fork, 0));
   int st = VK_OK;
-  // VK_FACTOR_TIMING=1 prints the device time of every size-class launch
+  // VK_FACTOR_TIMING=1 runs the classes one after another and prints the
+  // device time of each
   static const bool timing = getenv("VK_FACTOR_TIMING") != nullptr;
-  for (auto& bk : buckets) {
+  for (size_t c = 0; c < h->fac_classes.size() && !st; ++c) {
+    const int smax = std::get<0>(h->fac_classes[c]), first = std::get<1>(h->fac_classes[c]);
+    const int count = std::get<2>(h->fac_classes[c]);
+    cudaStream_t cs = (c == 0 || timing) ? cudaStream_t(0) : aux;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (timing && !bk.ids.empty()) {
+    if (timing) {
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       cudaEventRecord(e0, 0);
     }
-    st = launch_bucket(bk, h, a, d_status, nullptr, nullptr, 0, 0);
+    st = launch_class(smax, h->fac_ids + first, count, h, a, d_status, nullptr, nullptr, 0, cs);
     if (e0) {
       cudaEventRecord(e1, 0);
       cudaEventSynchronize(e1);
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e0, e1);
+      std::vector<int32_t> hid(count);
+      cudaMemcpy(hid.data(), h->fac_ids + first, sizeof(int32_t) * count, cudaMemcpyDeviceToHost);
       double f = 0.0;
-      for (int q : bk.ids) {
-        const double sz = double(h->h_off[q + 1] - h->h_off[q]);
-        f += 2.0 * sz * sz * sz / 3.0;
-      }
-      fprintf(stderr, "[vk_factor] class <=%d: %zu patches, %.3f ms (incl. id upload), %.1f GFLOP/s LU-equiv\n",
-              bk.smax, bk.ids.size(), ms, f / (ms * 1e-3) / 1e9);
+      for (int q : hid) f += 2.0 * std::pow(double(h->h_off[q + 1] - h->h_off[q]), 3) / 3.0;
+      fprintf(stderr, "[vk_factor] class <=%d: %d patches, %.3f ms, %.1f GFLOP/s LU-equiv\n",
+              smax, count, ms, f / (ms * 1e-3) / 1e9);
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
     }
-    if (st) break;
+  }
+  if (!st) {
+    VK_CHECK_CUDA(cudaEventRecord(ev_join, aux));
+    VK_CHECK_CUDA(cudaStreamWaitEvent(0, ev_join, 0));
   }
   std::vector<int32_t> hs(h->npatch);
   if (!st && h->npatch) {
@@ -713,7 +760,6 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
       st = VK_ERR_CUDA;
     }
   }
-  cudaFree(d_status);
   if (st) return st;
   if (status_host) std::copy(hs.begin(), hs.end(), status_host);
   int bad = -1;

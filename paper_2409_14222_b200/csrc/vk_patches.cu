@@ -231,6 +231,8 @@ void vk_patches_free(vk_patches_s* h) {
   cudaFree(h->dptr);
   cudaFree(h->dslot);
   cudaFree(h->zbuf);
+  cudaFree(h->fac_ids);
+  cudaFree(h->fac_status);
   delete h;
 }
 

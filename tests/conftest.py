@@ -33,8 +33,9 @@ def load_case(name):
         return _PACKS[name]
     from paper_2409_14222_b200.pack import read_pack
     pp, gp = case_paths(name)
-    if not os.path.exists(pp):
-        pytest.skip(f"{pp} not present (generate with tools/make_packs.py)")
+    for p in (pp, gp):
+        if not os.path.exists(p):
+            pytest.skip(f"{p} not present (generate with tools/make_packs.py)")
     g = dict(np.load(gp))
     hp = os.path.join(GOLDEN, f"{name}_history.json")
     if os.path.exists(hp):
