@@ -42,6 +42,7 @@ METRIC = "Vanka sweep patch-solves/s (P2/P1 256x256 finest level, damping 0.5)"
 UNIT = "patch-solves/s"
 CPU_SAMPLE_PATCHES = 4096
 E2E_MIN_STEPS = 100   # e2e pipeline steps (fill/drain amortised; >= --steps)
+FP64_PEAK_TFLOPS = 36.5  # measured DFMA peak on this B200 (profiles/r1_fp64_peak.json)
 
 
 def _env_int(name, default):
@@ -389,6 +390,51 @@ def run_ours(args):
     ms_res = q0.elapsed_time(q1) / 20
     bytes_res = 12 * A.nnz + 4 * (N + 1) + 24 * N
 
+    # ---- fine-level transfers (K6), each launch after a read-only 256 MB L2
+    # flush (the V-cycle runs them right after a residual streamed A through
+    # L2), with a device copy of the same byte count as the attainable floor
+    # for a one-shot stream of that size
+    tr = hier.transfers[len(hier.levels) - 1]
+    nf, nc = tr.P.shape
+    xc = torch.from_numpy(np.random.default_rng(3).uniform(-1.0, 1.0, nc)).to(dev)
+    flush = torch.ones(32 << 20, dtype=torch.float64, device=dev)
+    fsum = torch.empty((), dtype=torch.float64, device=dev)
+    b_pro = 12 * tr.P.nnz + 4 * (nf + 1) + 8 * (nf + nc) + 8 * nf
+    b_rst = 12 * tr.P.nnz + 4 * (nc + 1) + 8 * (nf + nc)
+    cs = torch.ones(b_pro // 16, dtype=torch.float64, device=dev)
+    cd = torch.empty_like(cs)
+
+    def cold_ms(fn, reps=20):
+        for _ in range(3):
+            fn()
+        pairs = []
+        for _ in range(reps):
+            torch.sum(flush, 0, out=fsum)
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            fn()
+            b_.record(stream)
+            pairs.append((a_, b_))
+        torch.cuda.synchronize()
+        return statistics.median(a_.elapsed_time(b_) for a_, b_ in pairs)
+
+    ms_pro = cold_ms(lambda: L.call("vk_spmv", tr.P.handle, L.ptr(xc), L.ptr(x), 1.0, 1.0, sp))
+    ms_rst = cold_ms(lambda: L.call("vk_spmv", tr.PT.handle, L.ptr(r), L.ptr(xc), 1.0, 0.0, sp))
+    ms_cpy = cold_ms(lambda: cd.copy_(cs))
+    del flush, cs, cd
+
+    # ---- K3 batched factorization of the fine level (re-factor: operator
+    # storage and schedule already built), LU-equivalent flops (2/3) sum s^3
+    fts = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        V.factor_patches(ps, fine.system)
+        torch.cuda.synchronize()
+        fts.append(time.perf_counter() - t0)
+    ms_fac = statistics.median(fts) * 1e3
+    flops_lu = (2.0 / 3.0) * float((sizes.astype(np.float64) ** 3).sum())
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -429,6 +475,21 @@ def run_ours(args):
                   "algorithmic_bytes": bytes_sweep},
         "residual_spmv": {"ms": ms_res, "gbps": bytes_res / (ms_res * 1e-3) / 1e9,
                           "nnz": int(A.nnz)},
+        "transfers": {
+            "note": "fine-level K6, one launch after an L2 flush, CUDA events; copy = device "
+                    "memcpy of the prolong byte count (attainable floor for a one-shot stream "
+                    "of this size)",
+            "prolong_add": {"ms": ms_pro, "gbps": b_pro / (ms_pro * 1e-3) / 1e9,
+                            "frac": b_pro / (ms_pro * 1e-3) / 1e9 / peak, "nnz": int(tr.P.nnz)},
+            "restrict": {"ms": ms_rst, "gbps": b_rst / (ms_rst * 1e-3) / 1e9,
+                         "frac": b_rst / (ms_rst * 1e-3) / 1e9 / peak},
+            "copy_same_bytes": {"ms": ms_cpy, "gbps": b_pro / (ms_cpy * 1e-3) / 1e9,
+                                "frac": b_pro / (ms_cpy * 1e-3) / 1e9 / peak}},
+        "factor": {"kernel": "K3 factor_tile_kernel (extraction + guard + Gauss-Jordan inverse)",
+                   "ms": ms_fac, "lu_equiv_gflop": flops_lu / 1e9,
+                   "tflops_lu_equiv": flops_lu / (ms_fac * 1e-3) / 1e12,
+                   "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+                   "frac_fp64_peak": flops_lu / (ms_fac * 1e-3) / 1e12 / FP64_PEAK_TFLOPS},
         "mg_fgmres": {"tts_ms_median": statistics.median(tts), "tts_ms": tts,
                       "iterations": its, "converged": bool(conv),
                       "reference_iterations": int(len(ref_hist) - 1) if ref_hist is not None else None,
