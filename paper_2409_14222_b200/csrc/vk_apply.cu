@@ -19,6 +19,23 @@
 
 namespace {
 
+#ifndef VK_GATHER_PDL  // K4b launched as a programmatic dependent of K4a
+#define VK_GATHER_PDL 0
+#endif
+#ifndef VK_GATHER_DPT  // DoFs per thread in K4b (independent chains in flight)
+#define VK_GATHER_DPT 1
+#endif
+
+// K4a kernels let the dependent K4b launch early: its CTAs become resident
+// beside the persistent K4a grid and wait in griddepcontrol.wait, so the
+// gather starts the moment the last patch operator has been applied.
+__device__ __forceinline__ void allow_dependent_launch() {
+#if VK_GATHER_PDL
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+}
+
+
 constexpr int kApplyWarps = 8;
 constexpr int kApplyMaxS = 192;
 
@@ -80,6 +97,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32, minb_of(RMAX)) patch_solve_k
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
+  allow_dependent_launch();
   __shared__ double rsh_all[kApplyWarps][32 * RMAX];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -161,20 +179,86 @@ __global__ void __launch_bounds__(kApplyWarps * 32, minb_of(RMAX)) patch_solve_k
   }
 }
 
+// K4b: thread per DoF (VK_GATHER_DPT DoFs per thread, interleaved by the
+// grid size so a resident grid covers all DoFs in one pass), slots read in
+// groups of four with the loads issued before the in-order additions —
+// acc = ((0 + z_0) + z_1) + ... in ascending patch order, exactly
+// out[idx] += ... of src/vanka.py:147.
 template <int MODE>
-__global__ void dof_gather_kernel(int ndof, const int* __restrict__ dptr, const int* __restrict__ dslot,
-                                  const double* __restrict__ z, double* __restrict__ out, double scale) {
-  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < ndof; d += gridDim.x * blockDim.x) {
-    const int k0 = dptr[d], k1 = dptr[d + 1];
-    double acc = 0.0;
-    for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, z[dslot[k]]);
-    if (MODE == VK_APPLY_OUT)
-      out[d] = acc;
-    else if (MODE == VK_APPLY_XSET)
-      out[d] = __dmul_rn(scale, acc);
-    else
-      out[d] = __dadd_rn(out[d], __dmul_rn(scale, acc));
+__global__ void __launch_bounds__(256) dof_gather_kernel(int ndof, const int* __restrict__ dptr,
+                                                         const int* __restrict__ dslot,
+                                                         const double* __restrict__ z,
+                                                         double* __restrict__ out, double scale) {
+#if VK_GATHER_PDL
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
+  constexpr int D = VK_GATHER_DPT;
+  const int nth = gridDim.x * blockDim.x;
+  for (int d0 = blockIdx.x * blockDim.x + threadIdx.x; d0 < ndof; d0 += D * nth) {
+    int a[D], e[D];
+    double acc[D];
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+      const int d = d0 + t * nth;
+      a[t] = 0;
+      e[t] = 0;
+      acc[t] = 0.0;
+      if (d < ndof) {
+        a[t] = dptr[d];
+        e[t] = dptr[d + 1];
+      }
+    }
+    for (int k = 0;; k += 4) {
+      bool any = false;
+#pragma unroll
+      for (int t = 0; t < D; ++t) any |= (a[t] + k < e[t]);
+      if (!any) break;
+      int sl[D][4];
+      double v[D][4];
+#pragma unroll
+      for (int t = 0; t < D; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sl[t][u] = (a[t] + k + u < e[t]) ? dslot[a[t] + k + u] : -1;
+#pragma unroll
+      for (int t = 0; t < D; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[t][u] = (sl[t][u] >= 0) ? z[sl[t][u]] : 0.0;
+#pragma unroll
+      for (int t = 0; t < D; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (sl[t][u] >= 0) acc[t] = __dadd_rn(acc[t], v[t][u]);
+    }
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+      const int d = d0 + t * nth;
+      if (d >= ndof) continue;
+      if (MODE == VK_APPLY_OUT)
+        out[d] = acc[t];
+      else if (MODE == VK_APPLY_XSET)
+        out[d] = __dmul_rn(scale, acc[t]);
+      else
+        out[d] = __dadd_rn(out[d], __dmul_rn(scale, acc[t]));
+    }
   }
+}
+
+template <int MODE>
+cudaError_t launch_gather(const vk_patches_s* h, double* out, double scale, cudaStream_t st) {
+  const int per_block = 256 * VK_GATHER_DPT;
+  const int grid = std::max(1, std::min((h->ndof + per_block - 1) / per_block, 148 * 8));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = VK_GATHER_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, dof_gather_kernel<MODE>, h->ndof, (const int*)h->dptr,
+                            (const int*)h->dslot, (const double*)h->zbuf, out, scale);
 }
 
 }  // namespace
@@ -198,6 +282,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_split_kernel(
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
+  allow_dependent_launch();
   constexpr int PPC = kApplyWarps / G;               // patches per CTA
   __shared__ double rsh[PPC][32 * R];
   __shared__ double part[PPC][G][32 * R];
@@ -270,6 +355,12 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_split_kernel(
 // same three-deep pipeline as patch_solve_kernel; per-element arithmetic is
 // identical (fma over columns in order, then fl(w*y)).
 constexpr int kBulkMaxS = 40;
+#ifndef VK_BULK_WPRE   // prefetch the weights with the residual gathers
+#define VK_BULK_WPRE 0
+#endif
+#ifndef VK_BULK_EARLY  // re-arm the freed stage before the z stores
+#define VK_BULK_EARLY 0
+#endif
 constexpr size_t kBulkMaxSmem =
     sizeof(double) * size_t((kBulkMaxS * kBulkMaxS + 1) & ~1) * 2 * kApplyWarps;
 
@@ -279,6 +370,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_bulk_kernel(
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z,
     int stage_doubles) {
+  allow_dependent_launch();
   extern __shared__ __align__(128) double sbuf[];   // [warps][2][stage_doubles]
   __shared__ __align__(8) uint64_t bars[kApplyWarps][2];
   __shared__ double rsh_all[kApplyWarps][32 * R];
@@ -307,7 +399,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_bulk_kernel(
   // pipeline registers: stage A (r values), B (indices), C (offsets)
   int64_t baseA = 0, opA = 0, baseB = 0, opB = 0, baseC = 0, opC = 0;
   int sA = 0, sB = 0, sC = 0;
-  double rA[R];
+  double rA[R], wA[R];   // r values and weights of the patch in stage A
   int iB[R];
   auto load_meta = [&](int p, int64_t& base, int& sz, int64_t& op) {
     if (p < npatch) {
@@ -326,6 +418,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_bulk_kernel(
   for (int q = 0; q < R; ++q) {
     const int i = lane + 32 * q;
     rA[q] = (i < sA) ? __ldg(r + idx[baseA + i]) : 0.0;
+    if (VK_BULK_WPRE) wA[q] = (i < sA) ? __ldg(w + baseA + i) : 0.0;
   }
   load_meta(p0 + nw, baseB, sB, opB);
   if (p0 + nw < npatch) issue(sB, opB, 1);
@@ -341,12 +434,17 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_bulk_kernel(
   for (int p = p0; p < npatch; p += nw) {
     const int64_t base = baseA;
     const int s = sA;
+    double wc[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) rsh[lane + 32 * q] = rA[q];
+    for (int q = 0; q < R; ++q) {
+      rsh[lane + 32 * q] = rA[q];
+      wc[q] = wA[q];
+    }
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const int i = lane + 32 * q;
       rA[q] = (i < sB) ? __ldg(r + iB[q]) : 0.0;
+      if (VK_BULK_WPRE) wA[q] = (i < sB) ? __ldg(w + baseB + i) : 0.0;
     }
     baseA = baseB; opA = opB; sA = sB;
 #pragma unroll
@@ -375,13 +473,19 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_bulk_kernel(
         if (R == 1 || i < s) y[q] = fma(A[j * s + i], rj, y[q]);
       }
     }
+    if (VK_BULK_EARLY) {
+      __syncwarp();                                 // stage b fully read: re-arm it
+      if (p + 2 * nw < npatch) issue(sN, opN, b);   // before the z stores
+    }
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const int i = lane + 32 * q;
-      if (i < s) z[base + i] = __dmul_rn(w[base + i], y[q]);
+      if (i < s) z[base + i] = __dmul_rn(VK_BULK_WPRE ? wc[q] : __ldg(w + base + i), y[q]);
     }
-    __syncwarp();                                   // stage b fully read
-    if (p + 2 * nw < npatch) issue(sN, opN, b);
+    if (!VK_BULK_EARLY) {
+      __syncwarp();                                 // stage b fully read
+      if (p + 2 * nw < npatch) issue(sN, opN, b);
+    }
     b ^= 1;
   }
 }
@@ -432,6 +536,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_chunk_kernel(
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
+  allow_dependent_launch();
   extern __shared__ __align__(128) double sbuf[];   // [warps][stages][kChunkDoubles]
   __shared__ __align__(8) uint64_t bars[kApplyWarps][kChunkStages];
   __shared__ double rsh_all[kApplyWarps][32 * RMAX];
@@ -484,7 +589,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_chunk_kernel(
   // residual pipeline (as patch_solve_kernel): A = r values, B = indices, C = offsets
   int64_t baseA = 0, baseB = 0, baseC = 0;
   int sA = 0, sB = 0, sC = 0;
-  double rA[RMAX];
+  double rA[RMAX], wA[RMAX];   // r values and weights of the patch in stage A
   int iB[RMAX];
   auto load_meta = [&](int p, int64_t& base, int& sz) {
     if (p < npatch) {
@@ -500,6 +605,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_chunk_kernel(
   for (int q = 0; q < RMAX; ++q) {
     const int i = lane + 32 * q;
     rA[q] = (i < sA) ? __ldg(r + idx[baseA + i]) : 0.0;
+    wA[q] = (i < sA) ? __ldg(w + baseA + i) : 0.0;
   }
   load_meta(p0 + nw, baseB, sB);
 #pragma unroll
@@ -514,12 +620,17 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_chunk_kernel(
   for (int p = p0; p < npatch; p += nw) {
     const int64_t base = baseA;
     const int s = sA;
+    double wc[RMAX];
 #pragma unroll
-    for (int q = 0; q < RMAX; ++q) rsh[lane + 32 * q] = rA[q];
+    for (int q = 0; q < RMAX; ++q) {
+      rsh[lane + 32 * q] = rA[q];
+      wc[q] = wA[q];
+    }
 #pragma unroll
     for (int q = 0; q < RMAX; ++q) {
       const int i = lane + 32 * q;
       rA[q] = (i < sB) ? __ldg(r + iB[q]) : 0.0;
+      wA[q] = (i < sB) ? __ldg(w + baseB + i) : 0.0;
     }
     baseA = baseB; sA = sB;
 #pragma unroll
@@ -550,7 +661,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_chunk_kernel(
 #pragma unroll
     for (int q = 0; q < RMAX; ++q) {
       const int i = lane + 32 * q;
-      if (i < s) z[base + i] = __dmul_rn(w[base + i], y[q]);
+      if (i < s) z[base + i] = __dmul_rn(wc[q], y[q]);
     }
   }
 }
@@ -669,18 +780,16 @@ extern "C" int vk_patches_accumulate(vk_patches_t h, double* out, double scale, 
   VK_REQUIRE(mode == VK_APPLY_OUT || mode == VK_APPLY_XSET || mode == VK_APPLY_XADD,
              "vk_patches_apply: bad mode %d", mode);
   cudaStream_t st = vk_stream(stream);
-  const int g2 = vk_grid(h->ndof, 256, 148 * 16);
   if (h->ndof > 0) {
+    cudaError_t e;
     switch (mode) {
-      case VK_APPLY_OUT:
-        dof_gather_kernel<VK_APPLY_OUT><<<g2, 256, 0, st>>>(h->ndof, h->dptr, h->dslot, h->zbuf, out, scale);
-        break;
-      case VK_APPLY_XSET:
-        dof_gather_kernel<VK_APPLY_XSET><<<g2, 256, 0, st>>>(h->ndof, h->dptr, h->dslot, h->zbuf, out, scale);
-        break;
-      default:
-        dof_gather_kernel<VK_APPLY_XADD><<<g2, 256, 0, st>>>(h->ndof, h->dptr, h->dslot, h->zbuf, out, scale);
-        break;
+      case VK_APPLY_OUT: e = launch_gather<VK_APPLY_OUT>(h, out, scale, st); break;
+      case VK_APPLY_XSET: e = launch_gather<VK_APPLY_XSET>(h, out, scale, st); break;
+      default: e = launch_gather<VK_APPLY_XADD>(h, out, scale, st); break;
+    }
+    if (e != cudaSuccess) {
+      vk::set_error("vk_patches_accumulate: %s", cudaGetErrorString(e));
+      return VK_ERR_CUDA;
     }
   }
   VK_CHECK_LAUNCH();
