@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(TR * TC, MB) factor_tile_kernel(
   __shared__ double prow[2][SM];
   __shared__ int sidx[SM], posof[SM], rowoff[SM + 1], rowk0[SM];
   __shared__ int wperm[NW][SM];            // per-warp copies of the position->row map
+  __shared__ int wpos[NW][SM];             // ... and of the row->position map
   __shared__ int s_bad;
   const int t = threadIdx.x;
   const int tr = t / TC, tc = t % TC;
@@ -363,7 +364,10 @@ __global__ void __launch_bounds__(TR * TC, MB) factor_tile_kernel(
       rowk0[i] = a0;
       rowoff[i + 1] = ptr[r + 1] - a0;
     }
-    for (int i = lane; i < s; i += 32) wperm[warp][i] = i;
+    for (int i = lane; i < s; i += 32) {
+      wperm[warp][i] = i;
+      wpos[warp][i] = i;
+    }
     for (int e = t; e < s * ld; e += NT) A[e] = 0.0;
     if (t == 0) s_bad = 0;
     __syncthreads();
@@ -405,14 +409,28 @@ __global__ void __launch_bounds__(TR * TC, MB) factor_tile_kernel(
         const int k = kb * TC + kt;
         if (k >= s || bad) break;
         const int buf = k & 1;
-        // pivot search (every warp): first max |colk| over positions k..s-1
+        // pivot search (every warp): first max |colk| over positions k..s-1,
+        // as a scan over rows (independent loads of position and value,
+        // lowest position kept among equal maxima — idamax's first max)
+        // (small blocks; large ones scan only the s - k open positions)
         double best = -1.0;
         int bi = s;
-        for (int q = k + lane; q < s; q += 32) {
-          const double v = fabs(colk[buf][wperm[warp][q]]);
-          if (v > best) {
-            best = v;
-            bi = q;
+        if constexpr (SM <= 64) {
+          for (int i = lane; i < s; i += 32) {
+            const int pi = wpos[warp][i];
+            const double v = fabs(colk[buf][i]);
+            if (pi >= k && (v > best || (v == best && pi < bi))) {
+              best = v;
+              bi = pi;
+            }
+          }
+        } else {
+          for (int q = k + lane; q < s; q += 32) {
+            const double v = fabs(colk[buf][wperm[warp][q]]);
+            if (v > best) {
+              best = v;
+              bi = q;
+            }
           }
         }
         const unsigned long long key =
@@ -428,6 +446,8 @@ __global__ void __launch_bounds__(TR * TC, MB) factor_tile_kernel(
         if (lane == 0) {
           wperm[warp][k] = r;
           wperm[warp][pos] = rk;
+          wpos[warp][r] = k;
+          wpos[warp][rk] = pos;
         }
         __syncwarp();
         const double piv = colk[buf][r];
