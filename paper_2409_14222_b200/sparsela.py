@@ -12,6 +12,7 @@ matrices (results come back as numpy) or CUDA ``torch.float64`` tensors /
 from __future__ import annotations
 
 import ctypes as C
+import time
 import weakref
 from dataclasses import dataclass
 
@@ -354,6 +355,11 @@ class FgmresWorkspace:
         g.replay()
 
 
+# tools/fgmres_profile.py sets this to a dict to collect per-iteration host
+# timings (graph launch call, wait for the Hessenberg column, Givens update)
+FGMRES_PROFILE = None
+
+
 def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
            nullspace=None, x0=None, target_norm=None, workspace: FgmresWorkspace | None = None):
     """Unrestarted flexible GMRES (reference ``sparsela.fgmres``,
@@ -441,12 +447,19 @@ def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
     converged = False
     breakdown = False
     j = 0
+    prof = FGMRES_PROFILE
     for j in range(max_it):
+        if prof is not None:
+            t0 = time.perf_counter()
         if ws is not None and ws.capturable(op, prec, proj):
             ws.replay(j, arnoldi_step, prec)       # one CUDA graph per Arnoldi step
         else:
             arnoldi_step(j, prec)
+        if prof is not None:
+            t1 = time.perf_counter()
         hs = scal.cpu().numpy()                                           # 1 sync
+        if prof is not None:
+            t2 = time.perf_counter()
         hess[:j + 2, j] = hs[:j + 2]
         wnorm0 = hs[max_it + 1]
         if hess[j + 1, j] <= 1e-14 * max(1.0, wnorm0):
@@ -464,6 +477,11 @@ def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
         g[j] = cs[j] * g[j]
         res = abs(g[j + 1])
         history.append(res / base)
+        if prof is not None:
+            t3 = time.perf_counter()
+            prof.setdefault("launch_s", []).append(t1 - t0)
+            prof.setdefault("sync_s", []).append(t2 - t1)
+            prof.setdefault("host_s", []).append(t3 - t2)
         if breakdown or res <= rtol * base:
             converged = True
             break
