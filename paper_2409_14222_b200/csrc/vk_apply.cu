@@ -355,112 +355,115 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_split_kernel(
 // same three-deep pipeline as patch_solve_kernel; per-element arithmetic is
 // identical (fma over columns in order, then fl(w*y)).
 constexpr int kBulkMaxS = 40;
-#ifndef VK_BULK_WPRE   // prefetch the weights with the residual gathers
-#define VK_BULK_WPRE 0
+#ifndef VK_BULK_NS     // stages (patch operators in flight) per warp
+#define VK_BULK_NS 2
 #endif
-#ifndef VK_BULK_EARLY  // re-arm the freed stage before the z stores
-#define VK_BULK_EARLY 0
+#ifndef VK_BULK_NW     // warps per CTA (one CTA per SM)
+#define VK_BULK_NW 8
 #endif
-constexpr size_t kBulkMaxSmem =
-    sizeof(double) * size_t((kBulkMaxS * kBulkMaxS + 1) & ~1) * 2 * kApplyWarps;
+constexpr int kBulkStages = VK_BULK_NS;
+constexpr int kBulkWarps = VK_BULK_NW;
+constexpr int kBulkDynMax = (227 - 8) * 1024;   // dynamic ring (static: gathers, barriers)
+inline size_t bulk_smem(int smax) {
+  return sizeof(double) * size_t((smax * smax + 1) & ~1) * kBulkStages * kBulkWarps;
+}
 
 template <int R>
-__global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_bulk_kernel(
+__global__ void __launch_bounds__(kBulkWarps * 32, 1) patch_solve_bulk_kernel(
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z,
     int stage_doubles) {
+  constexpr int NS = kBulkStages;
   allow_dependent_launch();
-  extern __shared__ __align__(128) double sbuf[];   // [warps][2][stage_doubles]
-  __shared__ __align__(8) uint64_t bars[kApplyWarps][2];
-  __shared__ double rsh_all[kApplyWarps][32 * R];
+  extern __shared__ __align__(128) double sbuf[];   // [warps][NS][stage_doubles]
+  __shared__ __align__(8) uint64_t bars[kBulkWarps][NS];
+  __shared__ double rsh_all[kBulkWarps][32 * R];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   double* rsh = rsh_all[warp];
-  double* stage[2] = {sbuf + (2 * warp) * stage_doubles, sbuf + (2 * warp + 1) * stage_doubles};
-  uint64_t* bar[2] = {&bars[warp][0], &bars[warp][1]};
-  const int nw = gridDim.x * kApplyWarps;
-  const int p0 = blockIdx.x * kApplyWarps + warp;
+  double* ring = sbuf + size_t(NS * warp) * stage_doubles;
+  uint64_t* bar = bars[warp];
+  const int nw = gridDim.x * kBulkWarps;
+  const int p0 = blockIdx.x * kBulkWarps + warp;
   if (lane == 0) {
-    mbar_init(bar[0], 1);
-    mbar_init(bar[1], 1);
+#pragma unroll
+    for (int q = 0; q < NS; ++q) mbar_init(&bar[q], 1);
     mbar_fence_init();
   }
   __syncwarp();
   const uint64_t pol = evict_first_policy();
-  auto issue = [&](int s, int64_t op, int b) {      // lane 0: patch operator -> stage b
+  auto issue = [&](int s, int64_t op, int st) {     // lane 0: patch operator -> stage st
     if (lane == 0) {
       const uint32_t bytes = static_cast<uint32_t>(((s * s + 1) & ~1) * sizeof(double));
-      mbar_expect_tx(bar[b], bytes);
-      bulk_g2s(stage[b], inv + op, bytes, bar[b], pol);
+      mbar_expect_tx(&bar[st], bytes);
+      bulk_g2s(ring + size_t(st) * stage_doubles, inv + op, bytes, &bar[st], pol);
     }
   };
+  auto meta_s = [&](int p) { return p < npatch ? static_cast<int>(off[p + 1] - off[p]) : 0; };
+  auto meta_op = [&](int p) { return p < npatch ? opoff[p] : int64_t(0); };
+  // fill the ring: patches p0, p0 + nw, ..., p0 + (NS-1) nw
+#pragma unroll
+  for (int q = 0; q < NS; ++q)
+    if (p0 + q * nw < npatch) issue(meta_s(p0 + q * nw), meta_op(p0 + q * nw), q);
+  // operator of the patch that refills the stage consumed next (p + NS nw),
+  // fetched one iteration ahead
+  int sI = meta_s(p0 + NS * nw);
+  int64_t opI = meta_op(p0 + NS * nw);
 
-  // pipeline registers: stage A (r values), B (indices), C (offsets)
-  int64_t baseA = 0, opA = 0, baseB = 0, opB = 0, baseC = 0, opC = 0;
+  // residual pipeline registers: stage A (r values), B (indices), C (offsets)
+  int64_t baseA = 0, baseB = 0, baseC = 0;
   int sA = 0, sB = 0, sC = 0;
-  double rA[R], wA[R];   // r values and weights of the patch in stage A
+  double rA[R];
   int iB[R];
-  auto load_meta = [&](int p, int64_t& base, int& sz, int64_t& op) {
+  auto load_meta = [&](int p, int64_t& base, int& sz) {
     if (p < npatch) {
       base = off[p];
       sz = static_cast<int>(off[p + 1] - base);
-      op = opoff[p];
     } else {
       base = 0;
       sz = 0;
-      op = 0;
     }
   };
-  load_meta(p0, baseA, sA, opA);
-  if (p0 < npatch) issue(sA, opA, 0);
+  load_meta(p0, baseA, sA);
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     const int i = lane + 32 * q;
     rA[q] = (i < sA) ? __ldg(r + idx[baseA + i]) : 0.0;
-    if (VK_BULK_WPRE) wA[q] = (i < sA) ? __ldg(w + baseA + i) : 0.0;
   }
-  load_meta(p0 + nw, baseB, sB, opB);
-  if (p0 + nw < npatch) issue(sB, opB, 1);
+  load_meta(p0 + nw, baseB, sB);
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     const int i = lane + 32 * q;
     iB[q] = (i < sB) ? idx[baseB + i] : 0;
   }
-  load_meta(p0 + 2 * nw, baseC, sC, opC);
+  load_meta(p0 + 2 * nw, baseC, sC);
 
-  uint32_t parity[2] = {0u, 0u};
+  uint32_t parity = 0u;                            // one bit per stage
   int b = 0;
   for (int p = p0; p < npatch; p += nw) {
     const int64_t base = baseA;
     const int s = sA;
-    double wc[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
-      rsh[lane + 32 * q] = rA[q];
-      wc[q] = wA[q];
-    }
+    for (int q = 0; q < R; ++q) rsh[lane + 32 * q] = rA[q];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const int i = lane + 32 * q;
       rA[q] = (i < sB) ? __ldg(r + iB[q]) : 0.0;
-      if (VK_BULK_WPRE) wA[q] = (i < sB) ? __ldg(w + baseB + i) : 0.0;
     }
-    baseA = baseB; opA = opB; sA = sB;
+    baseA = baseB; sA = sB;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const int i = lane + 32 * q;
       iB[q] = (i < sC) ? idx[baseC + i] : 0;
     }
-    const int sN = sC;
-    const int64_t opN = opC;
-    baseB = baseC; opB = opC; sB = sC;
-    load_meta(p + 3 * nw, baseC, sC, opC);
+    baseB = baseC; sB = sC;
+    load_meta(p + 3 * nw, baseC, sC);
     __syncwarp();
 
-    mbar_wait(bar[b], parity[b]);
-    parity[b] ^= 1u;
-    const double* A = stage[b];
+    mbar_wait(&bar[b], (parity >> b) & 1u);
+    parity ^= (1u << b);
+    const double* A = ring + size_t(b) * stage_doubles;
     double y[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) y[q] = 0.0;
@@ -473,20 +476,16 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_bulk_kernel(
         if (R == 1 || i < s) y[q] = fma(A[j * s + i], rj, y[q]);
       }
     }
-    if (VK_BULK_EARLY) {
-      __syncwarp();                                 // stage b fully read: re-arm it
-      if (p + 2 * nw < npatch) issue(sN, opN, b);   // before the z stores
-    }
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const int i = lane + 32 * q;
-      if (i < s) z[base + i] = __dmul_rn(VK_BULK_WPRE ? wc[q] : __ldg(w + base + i), y[q]);
+      if (i < s) z[base + i] = __dmul_rn(__ldg(w + base + i), y[q]);
     }
-    if (!VK_BULK_EARLY) {
-      __syncwarp();                                 // stage b fully read
-      if (p + 2 * nw < npatch) issue(sN, opN, b);
-    }
-    b ^= 1;
+    __syncwarp();                                   // stage b fully read
+    if (p + NS * nw < npatch) issue(sI, opI, b);
+    sI = meta_s(p + (NS + 1) * nw);
+    opI = meta_op(p + (NS + 1) * nw);
+    b = (b + 1 == NS) ? 0 : b + 1;
   }
 }
 
@@ -704,21 +703,22 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
       default: VK_SPLIT(4); break;
     }
 #undef VK_SPLIT
-  } else if (h->npatch > 0 && h->smax <= kBulkMaxS && !h->mixed_sizes && bulk_enabled()) {
-    // small patches: TMA bulk copies into a per-warp two-stage ring
+  } else if (h->npatch > 0 && h->smax <= kBulkMaxS && !h->mixed_sizes && bulk_enabled() &&
+             bulk_smem(h->smax) <= size_t(kBulkDynMax)) {
+    // small patches: TMA bulk copies into a per-warp ring of kBulkStages
     const int stage_doubles = ((h->smax * h->smax + 1) & ~1);
-    const size_t dsm = sizeof(double) * size_t(stage_doubles) * 2 * kApplyWarps;
-    const int want = (h->npatch + kApplyWarps - 1) / kApplyWarps;
+    const size_t dsm = bulk_smem(h->smax);
+    const int want = (h->npatch + kBulkWarps - 1) / kBulkWarps;
 #define VK_BULK(RV)                                                                           \
   do {                                                                                        \
     auto k = patch_solve_bulk_kernel<RV>;                                                     \
     static const cudaError_t attr = cudaFuncSetAttribute(                                     \
-        k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBulkMaxSmem));                   \
+        k, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkDynMax);                         \
     VK_CHECK_CUDA(attr);                                                                      \
-    const int grid = std::min(want, vk_resident_blocks((const void*)k, kApplyWarps * 32, dsm)); \
-    k<<<grid, kApplyWarps * 32, dsm, vk_stream(stream)>>>(h->npatch, h->off, h->idx, h->w,     \
-                                                         h->opoff, h->inv, r, h->zbuf,         \
-                                                         stage_doubles);                       \
+    const int grid = std::min(want, vk_resident_blocks((const void*)k, kBulkWarps * 32, dsm)); \
+    k<<<grid, kBulkWarps * 32, dsm, vk_stream(stream)>>>(h->npatch, h->off, h->idx, h->w,      \
+                                                        h->opoff, h->inv, r, h->zbuf,          \
+                                                        stage_doubles);                        \
   } while (0)
     if (rpl <= 1) VK_BULK(1);
     else VK_BULK(2);
