@@ -26,6 +26,8 @@ def main():
         hier.vcycle_device(b)
     torch.cuda.synchronize()
     ts = []
+    # under `ncu --profile-from-start off` only the timed replays are captured
+    torch.cuda.profiler.start()
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -33,6 +35,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
+    torch.cuda.profiler.stop()
     print(f"{name}: V-cycle graph {statistics.median(ts):.3f} ms; levels "
           f"{[lv.n for lv in hier.levels]}")
 
