@@ -19,21 +19,10 @@
 
 namespace {
 
-#ifndef VK_GATHER_PDL  // K4b launched as a programmatic dependent of K4a
-#define VK_GATHER_PDL 0
-#endif
 #ifndef VK_GATHER_DPT  // DoFs per thread in K4b (independent chains in flight)
 #define VK_GATHER_DPT 1
 #endif
 
-// K4a kernels let the dependent K4b launch early: its CTAs become resident
-// beside the persistent K4a grid and wait in griddepcontrol.wait, so the
-// gather starts the moment the last patch operator has been applied.
-__device__ __forceinline__ void allow_dependent_launch() {
-#if VK_GATHER_PDL
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-#endif
-}
 
 
 constexpr int kApplyWarps = 8;
@@ -97,7 +86,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32, minb_of(RMAX)) patch_solve_k
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
-  allow_dependent_launch();
+  pdl_trigger();
   __shared__ double rsh_all[kApplyWarps][32 * RMAX];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -122,6 +111,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32, minb_of(RMAX)) patch_solve_k
     }
   };
   load_meta(p0, baseA, sA, opA);
+  pdl_wait();   // operators / structure above are setup data; r is not
 #pragma unroll
   for (int q = 0; q < RMAX; ++q) {
     const int i = lane + 32 * q;
@@ -189,9 +179,8 @@ __global__ void __launch_bounds__(256) dof_gather_kernel(int ndof, const int* __
                                                          const int* __restrict__ dslot,
                                                          const double* __restrict__ z,
                                                          double* __restrict__ out, double scale) {
-#if VK_GATHER_PDL
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-#endif
+  pdl_trigger();
+  pdl_wait();
   constexpr int D = VK_GATHER_DPT;
   const int nth = gridDim.x * blockDim.x;
   for (int d0 = blockIdx.x * blockDim.x + threadIdx.x; d0 < ndof; d0 += D * nth) {
@@ -247,18 +236,9 @@ template <int MODE>
 cudaError_t launch_gather(const vk_patches_s* h, double* out, double scale, cudaStream_t st) {
   const int per_block = 256 * VK_GATHER_DPT;
   const int grid = std::max(1, std::min((h->ndof + per_block - 1) / per_block, 148 * 8));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = VK_GATHER_PDL;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, dof_gather_kernel<MODE>, h->ndof, (const int*)h->dptr,
-                            (const int*)h->dslot, (const double*)h->zbuf, out, scale);
+  return vk_launch(dof_gather_kernel<MODE>, dim3(grid), dim3(256), 0, st,
+                   12 * h->total + 16 * int64_t(h->ndof), h->ndof, (const int*)h->dptr,
+                   (const int*)h->dslot, (const double*)h->zbuf, out, scale);
 }
 
 }  // namespace
@@ -282,7 +262,8 @@ __global__ void __launch_bounds__(kApplyWarps * 32) patch_solve_split_kernel(
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
-  allow_dependent_launch();
+  pdl_trigger();
+  pdl_wait();
   constexpr int PPC = kApplyWarps / G;               // patches per CTA
   __shared__ double rsh[PPC][32 * R];
   __shared__ double part[PPC][G][32 * R];
@@ -375,7 +356,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1) patch_solve_bulk_kernel(
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z,
     int stage_doubles) {
   constexpr int NS = kBulkStages;
-  allow_dependent_launch();
+  pdl_trigger();
   extern __shared__ __align__(128) double sbuf[];   // [warps][NS][stage_doubles]
   __shared__ __align__(8) uint64_t bars[kBulkWarps][NS];
   __shared__ double rsh_all[kBulkWarps][32 * R];
@@ -426,6 +407,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1) patch_solve_bulk_kernel(
     }
   };
   load_meta(p0, baseA, sA);
+  pdl_wait();   // operators / structure above are setup data; r is not
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     const int i = lane + 32 * q;
@@ -535,7 +517,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_chunk_kernel(
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z) {
-  allow_dependent_launch();
+  pdl_trigger();
   extern __shared__ __align__(128) double sbuf[];   // [warps][stages][kChunkDoubles]
   __shared__ __align__(8) uint64_t bars[kApplyWarps][kChunkStages];
   __shared__ double rsh_all[kApplyWarps][32 * RMAX];
@@ -600,6 +582,7 @@ __global__ void __launch_bounds__(kApplyWarps * 32, 1) patch_solve_chunk_kernel(
     }
   };
   load_meta(p0, baseA, sA);
+  pdl_wait();   // operators / structure above are setup data; r is not
 #pragma unroll
   for (int q = 0; q < RMAX; ++q) {
     const int i = lane + 32 * q;
@@ -689,13 +672,16 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
   if (int st = check_apply(h)) return st;
   VK_REQUIRE(r, "vk_patches_solve: null residual");
   const int rpl = (h->smax + 31) / 32;
+  const int64_t bytes = 8 * h->inv_total + 20 * h->total;   // for the PDL decision
+  cudaError_t le = cudaSuccess;
   if (h->npatch > 0 && h->npatch < 148 * kApplyWarps * 4 && rpl <= 4) {
     // coarse levels: 4 warps per patch
     constexpr int G = 4;
     const int grid = std::min((h->npatch + kApplyWarps / G - 1) / (kApplyWarps / G), 148 * 16);
 #define VK_SPLIT(RV)                                                                        \
-  patch_solve_split_kernel<RV, G><<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(        \
-      h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf)
+  le = vk_launch(patch_solve_split_kernel<RV, G>, dim3(grid), dim3(kApplyWarps * 32), 0,    \
+                 vk_stream(stream), bytes, h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, \
+                 r, h->zbuf)
     switch (rpl) {
       case 1: VK_SPLIT(1); break;
       case 2: VK_SPLIT(2); break;
@@ -716,9 +702,9 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
         k, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkDynMax);                         \
     VK_CHECK_CUDA(attr);                                                                      \
     const int grid = std::min(want, vk_resident_blocks((const void*)k, kBulkWarps * 32, dsm)); \
-    k<<<grid, kBulkWarps * 32, dsm, vk_stream(stream)>>>(h->npatch, h->off, h->idx, h->w,      \
-                                                        h->opoff, h->inv, r, h->zbuf,          \
-                                                        stage_doubles);                        \
+    le = vk_launch(k, dim3(grid), dim3(kBulkWarps * 32), dsm, vk_stream(stream), bytes,       \
+                   h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf,             \
+                   stage_doubles);                                                            \
   } while (0)
     if (rpl <= 1) VK_BULK(1);
     else VK_BULK(2);
@@ -734,8 +720,8 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
         k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));                            \
     VK_CHECK_CUDA(attr);                                                                      \
     const int grid = std::min(want, vk_resident_blocks((const void*)k, kApplyWarps * 32, dsm)); \
-    k<<<grid, kApplyWarps * 32, dsm, vk_stream(stream)>>>(h->npatch, h->off, h->idx, h->w,     \
-                                                         h->opoff, h->inv, r, h->zbuf);        \
+    le = vk_launch(k, dim3(grid), dim3(kApplyWarps * 32), dsm, vk_stream(stream), bytes,      \
+                   h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf);            \
   } while (0)
     switch (rpl) {
       case 1: VK_CHUNK(1); break;
@@ -768,6 +754,10 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
       default: VK_SOLVE(6); break;
     }
 #undef VK_SOLVE
+  }
+  if (le != cudaSuccess) {
+    vk::set_error("vk_patches_solve: %s", cudaGetErrorString(le));
+    return VK_ERR_CUDA;
   }
   VK_CHECK_LAUNCH();
   return VK_OK;

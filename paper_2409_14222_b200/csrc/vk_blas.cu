@@ -33,6 +33,8 @@ template <int FIN>
 __global__ void __launch_bounds__(kRedBlock) dot_kernel(int64_t n, const double* __restrict__ x,
                                                         const double* __restrict__ y,
                                                         double* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double sh[kRedBlock];
   __shared__ bool last;
   double acc = 0.0;
@@ -67,6 +69,8 @@ __global__ void __launch_bounds__(kRedBlock) axpy_dot_kernel(int64_t n, const do
                                                              const double* __restrict__ x,
                                                              double* y, const double* x2,
                                                              double* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double sh[kRedBlock];
   __shared__ bool last;
   const double av = *a;
@@ -99,18 +103,24 @@ __global__ void __launch_bounds__(kRedBlock) axpy_dot_kernel(int64_t n, const do
 
 __global__ void axpy_dev_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ x,
                                 double* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
   const double av = *a;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     y[i] = __dsub_rn(y[i], __dmul_rn(av, x[i]));
 }
 
 __global__ void axpy_kernel(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     y[i] = __dadd_rn(y[i], __dmul_rn(a, x[i]));
 }
 
 __global__ void div_dev_kernel(int64_t n, const double* __restrict__ x, const double* __restrict__ d,
                                double* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
   const double dv = *d;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     y[i] = __ddiv_rn(x[i], dv);
@@ -118,6 +128,8 @@ __global__ void div_dev_kernel(int64_t n, const double* __restrict__ x, const do
 
 __global__ void copy_index_kernel(int64_t m, const int* __restrict__ idx, const double* __restrict__ src,
                                   double* __restrict__ dst) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < m; k += int64_t(gridDim.x) * blockDim.x) {
     const int i = idx[k];
     dst[i] = src[i];
@@ -127,6 +139,8 @@ __global__ void copy_index_kernel(int64_t m, const int* __restrict__ idx, const 
 // y = M x, dense row-major: one warp per row, 128-bit loads where aligned.
 __global__ void __launch_bounds__(256) gemv_kernel(int m, int n, const double* __restrict__ mat,
                                                    const double* __restrict__ x, double* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < m; row += nw) {
@@ -153,6 +167,8 @@ __global__ void __launch_bounds__(256) gemv_kernel(int m, int n, const double* _
 // x += sum_k c[k] * Z[k, :]  in ascending k
 __global__ void combine_kernel(int64_t n, int count, const double* __restrict__ z, const double* __restrict__ c,
                                double* __restrict__ x) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     double acc = 0.0;
     for (int k = 0; k < count; ++k) acc = fma(c[k], z[int64_t(k) * n + i], acc);
@@ -162,6 +178,8 @@ __global__ void combine_kernel(int64_t n, int count, const double* __restrict__ 
 
 __global__ void project_apply_kernel(int64_t n, const double* __restrict__ q, const double* __restrict__ s,
                                      double* __restrict__ x) {
+  pdl_trigger();
+  pdl_wait();
   const double sv = *s;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     x[i] = __dsub_rn(x[i], __dmul_rn(q[i], sv));
@@ -173,14 +191,14 @@ __global__ void project_apply_kernel(int64_t n, const double* __restrict__ q, co
 
 extern "C" int vk_dot(int64_t n, const double* x, const double* y, double* out_dev, void* stream) {
   VK_REQUIRE(out_dev && n >= 0 && (n == 0 || (x && y)), "vk_dot: bad argument");
-  dot_kernel<0><<<kRedGrid, kRedBlock, 0, vk_stream(stream)>>>(n, x, y, out_dev);
+  VK_CHECK_CUDA(vk_launch(dot_kernel<0>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 16 * n, n, x, y, out_dev));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
 
 extern "C" int vk_nrm2(int64_t n, const double* x, double* out_dev, void* stream) {
   VK_REQUIRE(out_dev && n >= 0 && (n == 0 || x), "vk_nrm2: bad argument");
-  dot_kernel<1><<<kRedGrid, kRedBlock, 0, vk_stream(stream)>>>(n, x, x, out_dev);
+  VK_CHECK_CUDA(vk_launch(dot_kernel<1>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 8 * n, n, x, x, out_dev));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
@@ -188,7 +206,7 @@ extern "C" int vk_nrm2(int64_t n, const double* x, double* out_dev, void* stream
 extern "C" int vk_axpy_dev(int64_t n, const double* a_dev, const double* x, double* y, void* stream) {
   VK_REQUIRE(a_dev && (n == 0 || (x && y)), "vk_axpy_dev: null argument");
   if (n == 0) return VK_OK;
-  axpy_dev_kernel<<<VK_VEC_GRID(n), 256, 0, vk_stream(stream)>>>(n, a_dev, x, y);
+  VK_CHECK_CUDA(vk_launch(axpy_dev_kernel, dim3(VK_VEC_GRID(n)), dim3(256), 0, vk_stream(stream), 24 * n, n, a_dev, x, y));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
@@ -197,9 +215,9 @@ extern "C" int vk_axpy_dot(int64_t n, const double* a_dev, const double* x, doub
                            double* out_dev, int32_t sqrt_out, void* stream) {
   VK_REQUIRE(a_dev && out_dev && n >= 0 && (n == 0 || (x && y && x2)), "vk_axpy_dot: bad argument");
   if (sqrt_out)
-    axpy_dot_kernel<1><<<kRedGrid, kRedBlock, 0, vk_stream(stream)>>>(n, a_dev, x, y, x2, out_dev);
+    VK_CHECK_CUDA(vk_launch(axpy_dot_kernel<1>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 8 * n, n, a_dev, x, y, x2, out_dev));
   else
-    axpy_dot_kernel<0><<<kRedGrid, kRedBlock, 0, vk_stream(stream)>>>(n, a_dev, x, y, x2, out_dev);
+    VK_CHECK_CUDA(vk_launch(axpy_dot_kernel<0>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 16 * n, n, a_dev, x, y, x2, out_dev));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
@@ -207,7 +225,7 @@ extern "C" int vk_axpy_dot(int64_t n, const double* a_dev, const double* x, doub
 extern "C" int vk_axpy(int64_t n, double a, const double* x, double* y, void* stream) {
   VK_REQUIRE(x && y, "vk_axpy: null argument");
   if (n == 0) return VK_OK;
-  axpy_kernel<<<VK_VEC_GRID(n), 256, 0, vk_stream(stream)>>>(n, a, x, y);
+  VK_CHECK_CUDA(vk_launch(axpy_kernel, dim3(VK_VEC_GRID(n)), dim3(256), 0, vk_stream(stream), 24 * n, n, a, x, y));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
@@ -215,7 +233,7 @@ extern "C" int vk_axpy(int64_t n, double a, const double* x, double* y, void* st
 extern "C" int vk_div_dev(int64_t n, const double* x, const double* d_dev, double* y, void* stream) {
   VK_REQUIRE(x && d_dev && y, "vk_div_dev: null argument");
   if (n == 0) return VK_OK;
-  div_dev_kernel<<<VK_VEC_GRID(n), 256, 0, vk_stream(stream)>>>(n, x, d_dev, y);
+  VK_CHECK_CUDA(vk_launch(div_dev_kernel, dim3(VK_VEC_GRID(n)), dim3(256), 0, vk_stream(stream), 16 * n, n, x, d_dev, y));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
@@ -223,8 +241,8 @@ extern "C" int vk_div_dev(int64_t n, const double* x, const double* d_dev, doubl
 extern "C" int vk_project(int64_t n, const double* q, double* x, double* scratch_dev, void* stream) {
   VK_REQUIRE(q && x && scratch_dev, "vk_project: null argument");
   if (n == 0) return VK_OK;
-  dot_kernel<0><<<kRedGrid, kRedBlock, 0, vk_stream(stream)>>>(n, q, x, scratch_dev);
-  project_apply_kernel<<<VK_VEC_GRID(n), 256, 0, vk_stream(stream)>>>(n, q, scratch_dev, x);
+  VK_CHECK_CUDA(vk_launch(dot_kernel<0>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 16 * n, n, q, x, scratch_dev));
+  VK_CHECK_CUDA(vk_launch(project_apply_kernel, dim3(VK_VEC_GRID(n)), dim3(256), 0, vk_stream(stream), 24 * n, n, q, scratch_dev, x));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
@@ -232,7 +250,7 @@ extern "C" int vk_project(int64_t n, const double* q, double* x, double* scratch
 extern "C" int vk_copy_index(int64_t m, const int32_t* idx, const double* src, double* dst, void* stream) {
   VK_REQUIRE(idx && src && dst, "vk_copy_index: null argument");
   if (m == 0) return VK_OK;
-  copy_index_kernel<<<VK_VEC_GRID(m), 256, 0, vk_stream(stream)>>>(m, idx, src, dst);
+  VK_CHECK_CUDA(vk_launch(copy_index_kernel, dim3(VK_VEC_GRID(m)), dim3(256), 0, vk_stream(stream), 20 * m, m, idx, src, dst));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
@@ -241,7 +259,7 @@ extern "C" int vk_gemv(int32_t m, int32_t n, const double* mat, const double* x,
   VK_REQUIRE(mat && x && y && m >= 0 && n >= 0, "vk_gemv: bad argument");
   if (m == 0) return VK_OK;
   const int grid = std::min((m + 7) / 8, 148 * 8);
-  gemv_kernel<<<grid, 256, 0, vk_stream(stream)>>>(m, n, mat, x, y);
+  VK_CHECK_CUDA(vk_launch(gemv_kernel, dim3(grid), dim3(256), 0, vk_stream(stream), 8 * int64_t(m) * n, m, n, mat, x, y));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
@@ -250,7 +268,7 @@ extern "C" int vk_combine(int64_t n, int32_t count, const double* z, const doubl
                           void* stream) {
   VK_REQUIRE(z && coef_dev && x, "vk_combine: null argument");
   if (n == 0 || count == 0) return VK_OK;
-  combine_kernel<<<VK_VEC_GRID(n), 256, 0, vk_stream(stream)>>>(n, count, z, coef_dev, x);
+  VK_CHECK_CUDA(vk_launch(combine_kernel, dim3(VK_VEC_GRID(n)), dim3(256), 0, vk_stream(stream), 8 * n * (int64_t(count) + 2), n, count, z, coef_dev, x));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }

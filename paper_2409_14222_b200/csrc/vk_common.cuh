@@ -4,12 +4,17 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
 #include <vector>
 
 #include "../../include/vanka_b200.h"
+
+#ifndef VK_PDL_MB_DEFAULT
+#define VK_PDL_MB_DEFAULT 0
+#endif
 
 namespace vk {
 
@@ -137,6 +142,48 @@ static inline int vk_resident_blocks(const void* kernel, int block, size_t smem 
 }
 
 // TMA 1-D bulk copies (cp.async.bulk) completed on an mbarrier.
+// ---- programmatic dependent launch (PDL) for the latency-bound coarse
+// levels.  Every kernel on the V-cycle path triggers its dependents at entry
+// (griddepcontrol.launch_dependents) and waits for its predecessor
+// (griddepcontrol.wait, a no-op without a programmatic predecessor) before
+// touching anything an earlier kernel in the stream produced; what it reads
+// before the wait is setup-time data (matrix / patch structure, operators).
+// The launch side opts in per launch: only launches that move less than
+// vk_pdl_bytes() (small, one-wave kernels) get the programmatic-serialisation
+// attribute, so big multi-wave kernels never share SMs with waiting CTAs.
+static __device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+static __device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+// bytes below which a launch may overlap its predecessor (VK_PDL_MB, MB;
+// 0 disables PDL)
+static inline int64_t vk_pdl_bytes() {
+  static const int64_t v = [] {
+    const char* e = getenv("VK_PDL_MB");
+    return int64_t(e ? atof(e) : VK_PDL_MB_DEFAULT) * (int64_t(1) << 20);
+  }();
+  return v;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t vk_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t st, int64_t bytes, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (bytes < vk_pdl_bytes()) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 static __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

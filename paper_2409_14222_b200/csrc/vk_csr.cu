@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
 #endif
   __shared__ double carry;
   const int t = threadIdx.x;
+  pdl_trigger();
   const int2 e0 = blk[blockIdx.x], e1 = blk[blockIdx.x + 1];
   const int r0 = e0.x, k0 = e0.y, k1 = e1.y;
   const int nr = e1.x - r0;
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
   // epilogue operand (b or y) of every row, staged by cp.async (no registers
   // held across the chunk loads)
 #if VK_CSR_PRE
+  pdl_wait();
   if (MODE == 1 || beta != 0.0) {
     const double* src = (MODE == 1) ? b : y;
     for (int i = t; i < nr; i += kStreamThreads) cp_async8(spre + i, src + r0 + i);
@@ -109,6 +111,9 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
 #define VK_PRE(i) ((MODE == 1) ? b[r0 + (i)] : y[r0 + (i)])
 #endif
   for (int i = t; i <= nr; i += kStreamThreads) cp_async4(sptr + i, ptr + r0 + i);
+  // block table and row pointers (setup data) are in flight; x and b / y
+  // come from the preceding kernel
+  pdl_wait();
   if (t == 0) carry = 0.0;
   for (int kc = k0; kc < k1 || (kc == k0 && k0 == k1); kc += kStreamNnz) {
     const int kend = min(k1, kc + kStreamNnz);
@@ -199,9 +204,14 @@ __global__ void __launch_bounds__(256) csr_row_kernel(
     int nrows, const int* __restrict__ ptr, const int* __restrict__ col,
     const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
     double alpha, double beta, const double* __restrict__ b) {
+  pdl_trigger();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= nrows) return;
+  if (row >= nrows) {
+    pdl_wait();
+    return;
+  }
   const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+  pdl_wait();
   double pre = 0.0;
   if (MODE == 1) pre = __ldg(b + row);
   else if (beta != 0.0) pre = y[row];
@@ -235,9 +245,9 @@ cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alp
                         const double* b, cudaStream_t st) {
   if (a.nblocks == 0) return cudaSuccess;
   if (a.warp_max_mean <= VK_CSR_SHORT) {
-    csr_row_kernel<MODE><<<(a.nrows + 255) / 256, 256, 0, st>>>(a.nrows, a.indptr, a.indices,
-                                                               a.data, x, y, alpha, beta, b);
-    return cudaGetLastError();
+    return vk_launch(csr_row_kernel<MODE>, dim3((a.nrows + 255) / 256), dim3(256), 0, st,
+                     12 * a.nnz + 24 * int64_t(a.nrows), a.nrows, a.indptr, a.indices, a.data,
+                     x, y, alpha, beta, b);
   }
 #if VK_CSR_CARVE
   static const cudaError_t carve = cudaFuncSetAttribute(
@@ -245,9 +255,9 @@ cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alp
       cudaSharedmemCarveoutMaxShared);
   if (carve != cudaSuccess) return carve;
 #endif
-  csr_stream_kernel<MODE><<<a.nblocks, kStreamThreads, 0, st>>>(a.blk, a.indptr, a.indices,
-                                                               a.data, x, y, alpha, beta, b);
-  return cudaGetLastError();
+  return vk_launch(csr_stream_kernel<MODE>, dim3(a.nblocks), dim3(kStreamThreads), 0, st,
+                   12 * a.nnz + 24 * int64_t(a.nrows), a.blk, a.indptr, a.indices, a.data, x, y,
+                   alpha, beta, b);
 }
 
 __global__ void csr_to_dense_kernel(int nrows, int ncols, const int* __restrict__ ptr,
