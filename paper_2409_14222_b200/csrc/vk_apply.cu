@@ -349,128 +349,19 @@ inline size_t bulk_smem(int smax) {
   return sizeof(double) * size_t((smax * smax + 1) & ~1) * kBulkStages * kBulkWarps;
 }
 
-// ---- fused sweep (VK_FUSED): K4b's DoF gather runs inside the bulk patch
-// kernel, a few rounds behind the patch stream.  Patch p is round p / nw of
-// warp p % nw; a DoF can be summed once the round of its last patch is
-// complete.  DoFs are pre-sorted by that round (gperm, offsets gro); each
-// warp publishes every finished round on a per-round counter (release) and
-// then sums its share of the DoFs of round k - kFuseLag (acquire on that
-// round's counter), in the reference's patch order (same operations as
-// dof_gather_kernel).  The grid is launched cooperatively (all CTAs
-// resident, so the waits cannot deadlock); the last warp out resets the
-// counters for the next launch.
-#ifndef VK_FUSED
-#define VK_FUSED 0
-#endif
-constexpr int kFuseLag = 2;
-constexpr int kFuseRot = 97;   // rotates the chunk -> warp assignment per round
-#ifndef VK_FUSE_PUBLANE        // lane that publishes a finished round
-#define VK_FUSE_PUBLANE 1
-#endif
-#ifndef VK_FUSE_SLEEP          // ns between polls of a round counter
-#define VK_FUSE_SLEEP 200
-#endif
-#ifndef VK_FUSE_DBG            // (timing experiments only; breaks the ordering)
-#define VK_FUSE_DBG 0
-#endif
-#ifndef VK_FUSE_GW             // dedicated gather warps per CTA (0: stream warps gather)
-#define VK_FUSE_GW 4
-#endif
-constexpr int kFuseGW = VK_FUSE_GW;
-constexpr int kFuseMaxRounds = 256;
-struct FuseArgs {
-  const int* gperm;        // DoFs sorted by completion round
-  const int* gro;          // [nrounds + 1]
-  unsigned* rdone;         // [nrounds] finished patches per round
-  unsigned* fin;           // warps done
-  const int* dptr;
-  const int* dslot;
-  double* out;
-  double scale;
-  int nrounds;
-};
-
-static __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-static __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-
-// gw / nwk: this worker warp and the number of worker warps sharing the
-// round's DoFs; nw: patch-stream warps (round rnd holds patches rnd*nw ...)
-template <int MODE>
-__device__ __forceinline__ void fuse_gather_round(const FuseArgs& fa, int rnd, int gw, int nwk,
-                                                  int lane, int npatch, const double* z, int nw) {
-  const int gb = fa.gro[rnd];
-  const int n_r = fa.gro[rnd + 1] - gb;
-  const int nch = (n_r + 31) >> 5;
-  int c = gw - static_cast<int>((static_cast<int64_t>(rnd) * kFuseRot) % nwk);
-  if (c < 0) c += nwk;
-  if (c >= nch) return;
-  const int inrnd = min(nw, npatch - rnd * nw);               // patches (warps) in the round
-  const unsigned target = static_cast<unsigned>((inrnd + kBulkWarps - 1) / kBulkWarps);  // CTAs
-#if VK_FUSE_DBG != 2
-  if (lane == 0)
-    while (ld_acquire_u32(fa.rdone + rnd) < target) __nanosleep(VK_FUSE_SLEEP);
-#endif
-  __syncwarp();
-  for (; c < nch; c += nwk) {
-    const int q = c * 32 + lane;
-    if (q < n_r) {
-      const int d = fa.gperm[gb + q];
-      const int k0 = fa.dptr[d], k1 = fa.dptr[d + 1];
-      double acc = 0.0;
-      for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, __ldcg(z + fa.dslot[k]));
-      if (MODE == VK_APPLY_OUT)
-        fa.out[d] = acc;
-      else if (MODE == VK_APPLY_XSET)
-        fa.out[d] = __dmul_rn(fa.scale, acc);
-      else
-        fa.out[d] = __dadd_rn(fa.out[d], __dmul_rn(fa.scale, acc));
-    }
-  }
-}
-
-template <int R, int FM = -1>
-__global__ void __launch_bounds__((kBulkWarps + (FM >= 0 ? kFuseGW : 0)) * 32, 1) patch_solve_bulk_kernel(
+template <int R>
+__global__ void __launch_bounds__(kBulkWarps * 32, 1) patch_solve_bulk_kernel(
     int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z,
-    int stage_doubles, FuseArgs fa) {
+    int stage_doubles) {
   constexpr int NS = kBulkStages;
   pdl_trigger();
   extern __shared__ __align__(128) double sbuf[];   // [warps][NS][stage_doubles]
   __shared__ __align__(8) uint64_t bars[kBulkWarps][NS];
   __shared__ double rsh_all[kBulkWarps][32 * R];
-  __shared__ unsigned cta_round[FM >= 0 ? kFuseMaxRounds : 1];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  if constexpr (FM >= 0) {
-    for (int i = threadIdx.x; i < kFuseMaxRounds; i += blockDim.x) cta_round[i] = 0u;
-    __syncthreads();
-  }
-  if constexpr (FM >= 0 && kFuseGW > 0) {
-    if (warp >= kBulkWarps) {                       // gather warp: rounds in order
-      pdl_wait();
-      const int ngw = gridDim.x * kFuseGW;
-      const int g = blockIdx.x * kFuseGW + (warp - kBulkWarps);
-      for (int rnd = 0; rnd < fa.nrounds; ++rnd)
-        fuse_gather_round<FM>(fa, rnd, g, ngw, lane, npatch, z, gridDim.x * kBulkWarps);
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        if (atomicAdd(fa.fin, 1u) == static_cast<unsigned>(ngw - 1)) {   // last gather warp out
-          for (int rnd = 0; rnd < fa.nrounds; ++rnd) fa.rdone[rnd] = 0u;
-          *fa.fin = 0u;
-          __threadfence();
-        }
-      }
-      return;
-    }
-  }
   double* rsh = rsh_all[warp];
   double* ring = sbuf + size_t(NS * warp) * stage_doubles;
   uint64_t* bar = bars[warp];
@@ -532,7 +423,6 @@ __global__ void __launch_bounds__((kBulkWarps + (FM >= 0 ? kFuseGW : 0)) * 32, 1
 
   uint32_t parity = 0u;                            // one bit per stage
   int b = 0;
-  int krnd = 0;                                    // this warp's round (fused sweep)
   for (int p = p0; p < npatch; p += nw) {
     const int64_t base = baseA;
     const int s = sA;
@@ -578,44 +468,6 @@ __global__ void __launch_bounds__((kBulkWarps + (FM >= 0 ? kFuseGW : 0)) * 32, 1
     sI = meta_s(p + (NS + 1) * nw);
     opI = meta_op(p + (NS + 1) * nw);
     b = (b + 1 == NS) ? 0 : b + 1;
-    if constexpr (FM >= 0) {
-#if VK_FUSE_DBG == 1
-      if (lane == 0) atomicAdd(fa.rdone + krnd, 1u);          // (timing experiment: relaxed)
-#elif VK_FUSE_DBG == 2
-      // (timing experiment: no publication)
-#else
-      // round krnd: this warp's z is stored.  The CTA's warps meet on a
-      // shared counter (acq_rel, CTA scope); the last of them publishes the
-      // CTA's round with one GPU-scope release (cumulative over the others'
-      // stores) — one global atomic per CTA and round instead of per warp.
-      if (lane == VK_FUSE_PUBLANE) {   // not lane 0: its fence would wait on its TMA copies
-        const int inrnd = min(kBulkWarps, npatch - krnd * nw - static_cast<int>(blockIdx.x) * kBulkWarps);
-        unsigned old;
-        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;\n"
-                     : "=r"(old) : "r"(smem_u32(&cta_round[krnd])) : "memory");
-        if (static_cast<int>(old) + 1 == inrnd) {
-          if (VK_FUSE_DBG == 3) atomicAdd(fa.rdone + krnd, 1u);   // (timing experiment)
-          else red_release_add(fa.rdone + krnd, 1u);
-        }
-      }
-#endif
-      if (kFuseGW == 0 && krnd >= kFuseLag)
-        fuse_gather_round<FM>(fa, krnd - kFuseLag, p0, nw, lane, npatch, z, nw);
-      ++krnd;
-    }
-  }
-  if constexpr (FM >= 0 && kFuseGW == 0) {
-    for (int rnd = max(0, krnd - kFuseLag); rnd < fa.nrounds; ++rnd)
-      fuse_gather_round<FM>(fa, rnd, p0, nw, lane, npatch, z, nw);
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence();
-      if (atomicAdd(fa.fin, 1u) == static_cast<unsigned>(nw - 1)) {   // last warp out
-        for (int rnd = 0; rnd < fa.nrounds; ++rnd) fa.rdone[rnd] = 0u;
-        *fa.fin = 0u;
-        __threadfence();
-      }
-    }
   }
 }
 
@@ -852,7 +704,7 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
     const int grid = std::min(want, vk_resident_blocks((const void*)k, kBulkWarps * 32, dsm)); \
     le = vk_launch(k, dim3(grid), dim3(kBulkWarps * 32), dsm, vk_stream(stream), bytes,       \
                    h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf,             \
-                   stage_doubles, FuseArgs{});                                                \
+                   stage_doubles);                                                            \
   } while (0)
     if (rpl <= 1) VK_BULK(1);
     else VK_BULK(2);
@@ -934,113 +786,9 @@ extern "C" int vk_patches_accumulate(vk_patches_t h, double* out, double scale, 
   return VK_OK;
 }
 
-namespace {
-
-// DoFs ordered by the round in which their last patch completes, for a grid
-// of nw warps (patch p = round p / nw).  Host-side, once per handle.
-int build_fuse_schedule(vk_patches_s* h, int nw) {
-  if (h->fus_nw == nw && h->fus_gperm) return VK_OK;
-  cudaFree(h->fus_gperm);
-  cudaFree(h->fus_gro);
-  cudaFree(h->fus_rdone);
-  h->fus_gperm = nullptr;
-  h->fus_gro = nullptr;
-  h->fus_rdone = nullptr;
-  const int n = h->ndof;
-  const int rounds = (h->npatch + nw - 1) / nw;
-  std::vector<int32_t> dp(n + 1), ds(h->total);
-  VK_CHECK_CUDA(cudaMemcpy(dp.data(), h->dptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost));
-  if (h->total)
-    VK_CHECK_CUDA(cudaMemcpy(ds.data(), h->dslot, sizeof(int32_t) * h->total, cudaMemcpyDeviceToHost));
-  std::vector<int32_t> rd(n, 0), gro(rounds + 1, 0), gperm(n);
-  for (int d = 0; d < n; ++d) {
-    if (dp[d + 1] > dp[d]) {
-      const int64_t slot = ds[dp[d + 1] - 1];
-      const int p = static_cast<int>(std::upper_bound(h->h_off.begin(), h->h_off.end(), slot) -
-                                     h->h_off.begin()) - 1;
-      rd[d] = p / nw;
-    }
-    gro[rd[d] + 1]++;
-  }
-  for (int k = 0; k < rounds; ++k) gro[k + 1] += gro[k];
-  std::vector<int32_t> cur(gro.begin(), gro.end() - 1);
-  for (int d = 0; d < n; ++d) gperm[cur[rd[d]]++] = d;
-  VK_CHECK_CUDA(cudaMalloc(&h->fus_gperm, sizeof(int32_t) * std::max(n, 1)));
-  VK_CHECK_CUDA(cudaMalloc(&h->fus_gro, sizeof(int32_t) * (rounds + 1)));
-  VK_CHECK_CUDA(cudaMalloc(&h->fus_rdone, sizeof(unsigned) * (rounds + 1)));
-  if (n) VK_CHECK_CUDA(cudaMemcpy(h->fus_gperm, gperm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
-  VK_CHECK_CUDA(cudaMemcpy(h->fus_gro, gro.data(), sizeof(int32_t) * (rounds + 1), cudaMemcpyHostToDevice));
-  VK_CHECK_CUDA(cudaMemset(h->fus_rdone, 0, sizeof(unsigned) * (rounds + 1)));
-  h->fus_nw = nw;
-  h->fus_rounds = rounds;
-  return VK_OK;
-}
-
-// 1 = launched, 0 = not applicable (caller falls back), < 0 = error
-template <int R, int FM>
-int launch_fused(vk_patches_s* h, const double* r, double* out, double scale, cudaStream_t st) {
-  auto k = patch_solve_bulk_kernel<R, FM>;
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkDynMax);
-  VK_CHECK_CUDA(attr);
-  const int stage_doubles = ((h->smax * h->smax + 1) & ~1);
-  const size_t dsm = bulk_smem(h->smax);
-  constexpr int threads = (kBulkWarps + kFuseGW) * 32;
-  const int grid = vk_resident_blocks((const void*)k, threads, dsm);
-  const int nw = grid * kBulkWarps;
-  if (grid < 1 || h->npatch < 4 * nw || (h->npatch + nw - 1) / nw > kFuseMaxRounds) return 0;
-  if (int e = build_fuse_schedule(h, nw)) return e;
-  FuseArgs fa{h->fus_gperm, h->fus_gro, h->fus_rdone, h->fus_rdone + h->fus_rounds,
-              h->dptr, h->dslot, out, scale, h->fus_rounds};
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = dsm;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;   // all CTAs resident: the round waits are safe
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  VK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k, h->npatch, (const int64_t*)h->off, (const int*)h->idx,
-                                   (const double*)h->w, (const int64_t*)h->opoff,
-                                   (const double*)h->inv, r, h->zbuf, stage_doubles, fa));
-  return 1;
-}
-
-static bool fused_enabled() {
-  static const bool v = [] {
-    const char* e = getenv("VK_FUSED");
-    return e ? e[0] != '0' : VK_FUSED != 0;
-  }();
-  return v;
-}
-
-}  // namespace
-
 extern "C" int vk_patches_apply(vk_patches_t h, const double* r, double* out, double scale,
                                 int32_t mode, void* stream) {
   VK_REQUIRE(r && out, "vk_patches_apply: null argument");
-  if (int st = check_apply(h)) return st;
-  VK_REQUIRE(mode == VK_APPLY_OUT || mode == VK_APPLY_XSET || mode == VK_APPLY_XADD,
-             "vk_patches_apply: bad mode %d", mode);
-  if (fused_enabled() && h->npatch > 0 && h->smax <= kBulkMaxS && !h->mixed_sizes &&
-      bulk_enabled() && bulk_smem(h->smax) <= size_t(kBulkDynMax)) {
-    const int rpl = (h->smax + 31) / 32;
-    cudaStream_t st = vk_stream(stream);
-    int done = 0;
-    if (rpl <= 1) {
-      done = mode == VK_APPLY_OUT  ? launch_fused<1, VK_APPLY_OUT>(h, r, out, scale, st)
-             : mode == VK_APPLY_XSET ? launch_fused<1, VK_APPLY_XSET>(h, r, out, scale, st)
-                                     : launch_fused<1, VK_APPLY_XADD>(h, r, out, scale, st);
-    } else {
-      done = mode == VK_APPLY_OUT  ? launch_fused<2, VK_APPLY_OUT>(h, r, out, scale, st)
-             : mode == VK_APPLY_XSET ? launch_fused<2, VK_APPLY_XSET>(h, r, out, scale, st)
-                                     : launch_fused<2, VK_APPLY_XADD>(h, r, out, scale, st);
-    }
-    if (done < 0) return done;
-    if (done == 1) return VK_OK;
-  }
   if (int st = vk_patches_solve(h, r, stream)) return st;
   return vk_patches_accumulate(h, out, scale, mode, stream);
 }

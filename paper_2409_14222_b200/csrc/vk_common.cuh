@@ -75,11 +75,6 @@ struct Patches {
   int32_t* fac_ids = nullptr;
   int32_t* fac_status = nullptr;  // [npatch]
   std::vector<std::tuple<int, int, int>> fac_classes;
-  // fused-sweep schedule (vk_apply.cu, VK_FUSED): DoFs by completion round
-  int fus_nw = 0, fus_rounds = 0;
-  int32_t* fus_gperm = nullptr;
-  int32_t* fus_gro = nullptr;
-  unsigned* fus_rdone = nullptr;  // [rounds + 1]; the last entry is the warps-done counter
 };
 
 }  // namespace vk

@@ -233,9 +233,6 @@ void vk_patches_free(vk_patches_s* h) {
   cudaFree(h->zbuf);
   cudaFree(h->fac_ids);
   cudaFree(h->fac_status);
-  cudaFree(h->fus_gperm);
-  cudaFree(h->fus_gro);
-  cudaFree(h->fus_rdone);
   delete h;
 }
 
