@@ -186,3 +186,30 @@ def test_fused_mgs_step_bit_identical(V, n):
         torch.cuda.synchronize()
         assert torch.equal(w1, w2)
         assert o1.cpu().numpy().view(np.uint64)[0] == o2.cpu().numpy().view(np.uint64)[0]
+
+
+@pytest.mark.parametrize("name", ["s_thtri2", "s_thtri4", "s_bdm3"])
+def test_refactor_reuses_schedule_and_tracks_values(V, name):
+    """Re-factorising a patch set (schedule and operator storage cached in
+    the handle, size classes on two streams) reproduces the first
+    factorisation bit for bit, and follows new matrix values: Gauss-Jordan
+    is exactly equivariant under a power-of-two scaling, so inv(2A) = inv(A)/2
+    to the last bit."""
+    import scipy.sparse as sp
+    from conftest import load_case
+    from paper_2409_14222_b200.vanka import patch_inverses
+    pack, _ = load_case(name)
+    lv = pack.fine
+    ps = V.factor_patches(V.build_patches(lv.mixed, lv.system.bc), lv.system)
+    n = ps.num_patches
+    pick = sorted({0, n // 3, n // 2, n - 1})
+    first = [patch_inverses(ps, p, 1)[0] for p in pick]
+    V.factor_patches(ps, lv.system)                       # same values again
+    again = [patch_inverses(ps, p, 1)[0] for p in pick]
+    for a, b in zip(first, again):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    a2 = sp.csr_matrix(lv.system.matrix * 2.0)
+    V.factor_patches(ps, a2)
+    halved = [patch_inverses(ps, p, 1)[0] for p in pick]
+    for a, h in zip(first, halved):
+        assert np.array_equal((a * 0.5).view(np.uint64), h.view(np.uint64))
