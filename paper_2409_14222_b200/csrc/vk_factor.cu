@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "vk_common.cuh"
@@ -697,6 +698,10 @@ extern "C" int vk_patches_extract(vk_patches_t h, vk_csr_t a, int32_t first, int
 
 extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_host, int32_t* first_bad) {
   VK_REQUIRE(h && a, "vk_patches_factor: null argument");
+  // setup-time call: serialised, because the auxiliary stream and its
+  // fork/join events below are shared by all handles
+  static std::mutex factor_mutex;
+  std::lock_guard<std::mutex> lock(factor_mutex);
   VK_REQUIRE(a->nrows == h->ndof && a->ncols == h->ndof,
              "vk_patches_factor: matrix is %dx%d, patches need %d", a->nrows, a->ncols, h->ndof);
   if (h->smax > kMaxPatch) {
@@ -743,13 +748,20 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
   int* d_status = h->fac_status;
   // The largest class (most work) runs on the legacy stream, the small ones
   // (boundary / coarse patches) beside it on an auxiliary stream; one join.
-  static cudaStream_t aux = nullptr;
-  static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (!aux) {
-    VK_CHECK_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
-    VK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    VK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-  }
+  struct AuxStream {                 // created once, thread-safe (function-local static)
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaError_t err = cudaSuccess;
+    AuxStream() {
+      err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      if (err == cudaSuccess) err = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+      if (err == cudaSuccess) err = cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    }
+  };
+  static AuxStream aux_streams;
+  VK_CHECK_CUDA(aux_streams.err);
+  cudaStream_t aux = aux_streams.s;
+  cudaEvent_t ev_fork = aux_streams.fork, ev_join = aux_streams.join;
   VK_CHECK_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int) * std::max(h->npatch, 1), 0));
   VK_CHECK_CUDA(cudaEventRecord(ev_fork, 0));
   VK_CHECK_CUDA(cudaStreamWaitEvent(aux, ev_fork, 0));
