@@ -18,6 +18,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--hier", action="store_true", help="use the patches of a full 5-level hierarchy")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -26,7 +27,10 @@ def main():
     from paper_2409_14222_b200.pack import read_pack
     pack = read_pack(os.path.join(ROOT, "data", "cfg2_pack.npz"))
     lv = pack.fine
-    ps = V.factor_patches(V.build_patches(lv.mixed, lv.system.bc), lv.system)
+    if args.hier:
+        ps = V.hierarchy_from_pack(pack).fine.patches
+    else:
+        ps = V.factor_patches(V.build_patches(lv.mixed, lv.system.bc), lv.system)
     n = lv.system.matrix.shape[0]
     st = torch.cuda.current_stream()
     r_host = [torch.from_numpy(np.random.default_rng(10 + i).uniform(-1, 1, n)).pin_memory()
