@@ -19,9 +19,6 @@
 
 namespace {
 
-#ifndef VK_GATHER_DPT  // DoFs per thread in K4b (independent chains in flight)
-#define VK_GATHER_DPT 1
-#endif
 
 
 
@@ -169,11 +166,10 @@ __global__ void __launch_bounds__(kApplyWarps * 32, minb_of(RMAX)) patch_solve_k
   }
 }
 
-// K4b: thread per DoF (VK_GATHER_DPT DoFs per thread, interleaved by the
-// grid size so a resident grid covers all DoFs in one pass), slots read in
-// groups of four with the loads issued before the in-order additions —
-// acc = ((0 + z_0) + z_1) + ... in ascending patch order, exactly
-// out[idx] += ... of src/vanka.py:147.
+// K4b: thread per DoF, its slots read in groups of four with the loads
+// issued before the in-order additions — acc = ((0 + z_0) + z_1) + ... in
+// ascending patch order, exactly out[idx] += ... of src/vanka.py:147.  (Two
+// DoFs per thread in one resident wave measured slower.)
 template <int MODE>
 __global__ void __launch_bounds__(256) dof_gather_kernel(int ndof, const int* __restrict__ dptr,
                                                          const int* __restrict__ dslot,
@@ -181,61 +177,33 @@ __global__ void __launch_bounds__(256) dof_gather_kernel(int ndof, const int* __
                                                          double* __restrict__ out, double scale) {
   pdl_trigger();
   pdl_wait();
-  constexpr int D = VK_GATHER_DPT;
   const int nth = gridDim.x * blockDim.x;
-  for (int d0 = blockIdx.x * blockDim.x + threadIdx.x; d0 < ndof; d0 += D * nth) {
-    int a[D], e[D];
-    double acc[D];
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < ndof; d += nth) {
+    const int a = dptr[d], e = dptr[d + 1];
+    double acc = 0.0;
+    for (int k = a; k < e; k += 4) {
+      int sl[4];
+      double v[4];
 #pragma unroll
-    for (int t = 0; t < D; ++t) {
-      const int d = d0 + t * nth;
-      a[t] = 0;
-      e[t] = 0;
-      acc[t] = 0.0;
-      if (d < ndof) {
-        a[t] = dptr[d];
-        e[t] = dptr[d + 1];
-      }
+      for (int u = 0; u < 4; ++u) sl[u] = (k + u < e) ? dslot[k + u] : -1;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = (sl[u] >= 0) ? z[sl[u]] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (sl[u] >= 0) acc = __dadd_rn(acc, v[u]);
     }
-    for (int k = 0;; k += 4) {
-      bool any = false;
-#pragma unroll
-      for (int t = 0; t < D; ++t) any |= (a[t] + k < e[t]);
-      if (!any) break;
-      int sl[D][4];
-      double v[D][4];
-#pragma unroll
-      for (int t = 0; t < D; ++t)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) sl[t][u] = (a[t] + k + u < e[t]) ? dslot[a[t] + k + u] : -1;
-#pragma unroll
-      for (int t = 0; t < D; ++t)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[t][u] = (sl[t][u] >= 0) ? z[sl[t][u]] : 0.0;
-#pragma unroll
-      for (int t = 0; t < D; ++t)
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (sl[t][u] >= 0) acc[t] = __dadd_rn(acc[t], v[t][u]);
-    }
-#pragma unroll
-    for (int t = 0; t < D; ++t) {
-      const int d = d0 + t * nth;
-      if (d >= ndof) continue;
-      if (MODE == VK_APPLY_OUT)
-        out[d] = acc[t];
-      else if (MODE == VK_APPLY_XSET)
-        out[d] = __dmul_rn(scale, acc[t]);
-      else
-        out[d] = __dadd_rn(out[d], __dmul_rn(scale, acc[t]));
-    }
+    if (MODE == VK_APPLY_OUT)
+      out[d] = acc;
+    else if (MODE == VK_APPLY_XSET)
+      out[d] = __dmul_rn(scale, acc);
+    else
+      out[d] = __dadd_rn(out[d], __dmul_rn(scale, acc));
   }
 }
 
 template <int MODE>
 cudaError_t launch_gather(const vk_patches_s* h, double* out, double scale, cudaStream_t st) {
-  const int per_block = 256 * VK_GATHER_DPT;
-  const int grid = std::max(1, std::min((h->ndof + per_block - 1) / per_block, 148 * 8));
+  const int grid = std::max(1, std::min((h->ndof + 255) / 256, 148 * 8));
   return vk_launch(dof_gather_kernel<MODE>, dim3(grid), dim3(256), 0, st,
                    12 * h->total + 16 * int64_t(h->ndof), h->ndof, (const int*)h->dptr,
                    (const int*)h->dslot, (const double*)h->zbuf, out, scale);

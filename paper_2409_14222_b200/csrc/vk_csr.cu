@@ -21,17 +21,8 @@
 
 #include "vk_common.cuh"
 
-#ifndef VK_CSR_SKEW
-#define VK_CSR_SKEW 1
-#endif
-#ifndef VK_CSR_PRE  // (experiment) stage b / y rows in shared memory by cp.async
-#define VK_CSR_PRE 0
-#endif
 #ifndef VK_CSR_SHORT  // thread-per-row kernel when the mean over 32-row groups of
 #define VK_CSR_SHORT 11  // the longest row is <= this (measured: transfers P of cfg2/3)
-#endif
-#ifndef VK_CSR_CARVE  // (experiment) force the max-shared carveout
-#define VK_CSR_CARVE 0
 #endif
 
 namespace vk {
@@ -65,12 +56,6 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
 }
-#if VK_CSR_PRE
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
-}
-#endif
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
@@ -88,9 +73,6 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
     double alpha, double beta, const double* __restrict__ b) {
   __shared__ double prod[kStreamNnz];
   __shared__ int sptr[kStreamRows + 1];
-#if VK_CSR_PRE
-  __shared__ double spre[kStreamRows];
-#endif
   __shared__ double carry;
   const int t = threadIdx.x;
   pdl_trigger();
@@ -98,18 +80,8 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
   const int r0 = e0.x, k0 = e0.y, k1 = e1.y;
   const int nr = e1.x - r0;
   const bool single = (nr == 1);
-  // epilogue operand (b or y) of every row, staged by cp.async (no registers
-  // held across the chunk loads)
-#if VK_CSR_PRE
-  pdl_wait();
-  if (MODE == 1 || beta != 0.0) {
-    const double* src = (MODE == 1) ? b : y;
-    for (int i = t; i < nr; i += kStreamThreads) cp_async8(spre + i, src + r0 + i);
-  }
-#define VK_PRE(i) spre[i]
-#else
+  // epilogue operand (b or y) of each row, read after its sum
 #define VK_PRE(i) ((MODE == 1) ? b[r0 + (i)] : y[r0 + (i)])
-#endif
   for (int i = t; i <= nr; i += kStreamThreads) cp_async4(sptr + i, ptr + r0 + i);
   // block table and row pointers (setup data) are in flight; x and b / y
   // come from the preceding kernel
@@ -140,12 +112,12 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
         carry = s;
       }
     } else {
-      // One thread per row, each row summed left to right.  Rows whose
-      // starts fall in the same 8-byte bank slot (within a half-warp) would
-      // serialise every shared-memory step; lane l therefore starts d steps
-      // late, d = its rank among the half-warp lanes sharing its start slot,
-      // which spreads a g-way collision over g consecutive slots at a cost of
-      // g - 1 extra steps (0 for conflict-free starts such as short rows).
+      // One thread per row, each row summed left to right.  Lane l starts
+      // d = (a - l) mod 16 steps late, so at every step the half-warp reads
+      // 16 distinct 8-byte bank slots ((a + k) mod 16 == (step + l) mod 16)
+      // instead of colliding whenever row starts agree mod 16.  (A cheaper
+      // skew — d = rank among the lanes sharing a start slot — and no skew
+      // measured slower.)
       for (int i0 = 0; i0 < nr; i0 += kStreamThreads) {
         const int i = i0 + t;
         const int lane = t & 31;
@@ -154,15 +126,7 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
           a = sptr[i] - kc;
           len = sptr[i + 1] - kc - a;
         }
-#if VK_CSR_SKEW == 1  // (experiment) full skew: every lane d = (a - l) mod 16
         const int d = len > 0 ? (a - lane) & 15 : 0;
-#elif VK_CSR_SKEW == 0  // (experiment) no skew
-        const int d = 0;
-#else
-        const int key = len > 0 ? ((a & 15) | (lane & 16)) : 32 + lane;
-        const unsigned same = __match_any_sync(0xffffffffu, key);
-        const int d = __popc(same & ((1u << lane) - 1u));
-#endif
         const int steps = __reduce_max_sync(0xffffffffu, len > 0 ? len + d : 0);
         double s = 0.0;
 #pragma unroll 4
@@ -195,6 +159,8 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
     }
   }
 }
+
+#undef VK_PRE
 
 // Short-row kernel (thread per row): for matrices with a few nonzeros per
 // row (prolongations) the shared-memory staging of the stream kernel costs
@@ -249,12 +215,6 @@ cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alp
                      12 * a.nnz + 24 * int64_t(a.nrows), a.nrows, a.indptr, a.indices, a.data,
                      x, y, alpha, beta, b);
   }
-#if VK_CSR_CARVE
-  static const cudaError_t carve = cudaFuncSetAttribute(
-      csr_stream_kernel<MODE>, cudaFuncAttributePreferredSharedMemoryCarveout,
-      cudaSharedmemCarveoutMaxShared);
-  if (carve != cudaSuccess) return carve;
-#endif
   return vk_launch(csr_stream_kernel<MODE>, dim3(a.nblocks), dim3(kStreamThreads), 0, st,
                    12 * a.nnz + 24 * int64_t(a.nrows), a.blk, a.indptr, a.indices, a.data, x, y,
                    alpha, beta, b);

@@ -329,16 +329,6 @@ std::vector<Bucket> make_buckets(const std::vector<int64_t>& off, int first, int
 // a*rinv (rinv in the pivot column), update fma(-f, p_j, a) (-f*rinv in the
 // pivot column).  The inverse Ainv[i][j] = Y[perm[i]][iperm[j]] is scattered
 // straight from the registers to the column-major operator.
-// (experiment) s <= 40 class shape: 0 = 8x8 threads x 5x5 tile (default),
-// 1 = 8x16 x 5x3, 2 = 8x4 x 5x10 (one warp per patch).  cfg2 re-factor:
-// 3.64 / 4.35 (6 CTAs/SM) / 4.29 ms (12 CTAs/SM) — more threads per patch pay
-// in barriers and redundant pivot searches, fewer in registers/occupancy.
-#ifndef VK_TILE40
-#define VK_TILE40 0
-#endif
-#ifndef VK_TILE40_MB
-#define VK_TILE40_MB 6
-#endif
 template <int TR, int TC, int RA, int CB, int MB>
 __global__ void __launch_bounds__(TR * TC, MB) factor_tile_kernel(
     const int* __restrict__ plist, int count, const int64_t* __restrict__ off,
@@ -579,11 +569,7 @@ int launch_class(int smax, const int* d_ids, int count, const vk_patches_s* h, c
     if (smax <= 16) VK_TILE(8, 8, 2, 2, 8);
     else if (smax <= 24) VK_TILE(8, 8, 3, 3, 8);
     else if (smax <= 32) VK_TILE(8, 8, 4, 4, 8);
-    else if (smax <= 40) {
-      if (VK_TILE40 == 1) VK_TILE(8, 16, 5, 3, VK_TILE40_MB);
-      else if (VK_TILE40 == 2) VK_TILE(8, 4, 5, 10, VK_TILE40_MB);
-      else VK_TILE(8, 8, 5, 5, 8);
-    }
+    else if (smax <= 40) VK_TILE(8, 8, 5, 5, 8);   // 8x16 x 5x3, 8x4 x 5x10: slower
     else if (smax <= 48) VK_TILE(8, 8, 6, 6, 8);
     else if (smax <= 56) VK_TILE(8, 8, 7, 7, 6);
     else if (smax <= 64) VK_TILE(8, 16, 8, 4, 4);
