@@ -15,6 +15,7 @@
 // bit-identical to the reference.
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -206,10 +207,73 @@ __global__ void __launch_bounds__(256) csr_row_kernel(
   }
 }
 
+// Opt-in tree-reduction kernel (VK_SPMV_TREE=1, NOT bit-exact): G lanes
+// per row stride over its entries with FMA and combine by a shuffle tree —
+// the usual vector-CSR SpMV.  It trades scipy's sequential, FMA-free row
+// order (hence bit-identity with the reference) for parallel row sums; it
+// exists to measure what that order costs.  The bit-exact kernels above stay
+// the default everywhere.
+template <int MODE, int G>
+__global__ void __launch_bounds__(256) csr_tree_kernel(
+    int nrows, const int* __restrict__ ptr, const int* __restrict__ col,
+    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+    double alpha, double beta, const double* __restrict__ b) {
+  pdl_trigger();
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % G;
+  const int rows_per_cta = blockDim.x / G;
+  for (int row0 = blockIdx.x * rows_per_cta; row0 < nrows; row0 += gridDim.x * rows_per_cta) {
+    const int row = row0 + threadIdx.x / G;
+    double s = 0.0;
+    if (row < nrows) {
+      const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
+      for (int k = k0 + sub; k < k1; k += G) s = fma(__ldcs(val + k), __ldg(x + __ldcs(col + k)), s);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
+    if (row < nrows && sub == 0) {
+      if (MODE == 1) {
+        y[row] = b[row] - s;
+      } else {
+        double out = alpha * s;
+        if (beta != 0.0) out += beta * y[row];
+        y[row] = out;
+      }
+    }
+  }
+}
+
+static bool tree_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("VK_SPMV_TREE");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+template <int MODE>
+cudaError_t launch_tree(const vk::Csr& a, const double* x, double* y, double alpha, double beta,
+                        const double* b, cudaStream_t st) {
+  const double m = a.mean_row;
+  const int64_t bytes = 12 * a.nnz + 24 * int64_t(a.nrows);
+#define VK_TREE(G_)                                                                             \
+  return vk_launch(csr_tree_kernel<MODE, G_>, dim3(std::min<int64_t>((a.nrows + 256 / G_ - 1) /  \
+                                                                     (256 / G_), 148 * 16)),     \
+                   dim3(256), 0, st, bytes, a.nrows, a.indptr, a.indices, a.data, x, y, alpha,    \
+                   beta, b)
+  if (m <= 12) VK_TREE(4);
+  if (m <= 24) VK_TREE(8);
+  if (m <= 48) VK_TREE(16);
+  VK_TREE(32);
+#undef VK_TREE
+}
+
 template <int MODE>
 cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alpha, double beta,
                         const double* b, cudaStream_t st) {
   if (a.nblocks == 0) return cudaSuccess;
+  if (tree_enabled()) return launch_tree<MODE>(a, x, y, alpha, beta, b, st);
   if (a.warp_max_mean <= VK_CSR_SHORT) {
     return vk_launch(csr_row_kernel<MODE>, dim3((a.nrows + 255) / 256), dim3(256), 0, st,
                      12 * a.nnz + 24 * int64_t(a.nrows), a.nrows, a.indptr, a.indices, a.data,
