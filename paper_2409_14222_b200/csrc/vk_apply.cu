@@ -201,41 +201,6 @@ __global__ void __launch_bounds__(256) dof_gather_kernel(int ndof, const int* __
   }
 }
 
-// K4b over a DoF list (the two halves of the overlapped sweep); the same
-// per-DoF operations as dof_gather_kernel.
-template <int MODE>
-__global__ void __launch_bounds__(256) dof_gather_list_kernel(int n, const int* __restrict__ list,
-                                                              const int* __restrict__ dptr,
-                                                              const int* __restrict__ dslot,
-                                                              const double* __restrict__ z,
-                                                              double* __restrict__ out, double scale) {
-  pdl_trigger();
-  pdl_wait();
-  const int nth = gridDim.x * blockDim.x;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += nth) {
-    const int d = list[q];
-    const int a = dptr[d], e = dptr[d + 1];
-    double acc = 0.0;
-    for (int k = a; k < e; k += 4) {
-      int sl[4];
-      double v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) sl[u] = (k + u < e) ? dslot[k + u] : -1;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = (sl[u] >= 0) ? z[sl[u]] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (sl[u] >= 0) acc = __dadd_rn(acc, v[u]);
-    }
-    if (MODE == VK_APPLY_OUT)
-      out[d] = acc;
-    else if (MODE == VK_APPLY_XSET)
-      out[d] = __dmul_rn(scale, acc);
-    else
-      out[d] = __dadd_rn(out[d], __dmul_rn(scale, acc));
-  }
-}
-
 template <int MODE>
 cudaError_t launch_gather(const vk_patches_s* h, double* out, double scale, cudaStream_t st) {
   const int grid = std::max(1, std::min((h->ndof + 255) / 256, 148 * 8));
@@ -346,9 +311,6 @@ constexpr int kBulkMaxS = 40;
 #define VK_BULK_NW 8
 #endif
 constexpr int kBulkStages = VK_BULK_NS;
-#ifndef VK_SWEEP_SPLIT   // percent of patches before the overlap point (0: plain sweep)
-#define VK_SWEEP_SPLIT 0
-#endif
 constexpr int kBulkWarps = VK_BULK_NW;
 constexpr int kBulkDynMax = (227 - 8) * 1024;   // dynamic ring (static: gathers, barriers)
 inline size_t bulk_smem(int smax) {
@@ -357,7 +319,7 @@ inline size_t bulk_smem(int smax) {
 
 template <int R>
 __global__ void __launch_bounds__(kBulkWarps * 32, 1) patch_solve_bulk_kernel(
-    int pfirst, int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
+    int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
     const double* __restrict__ w, const int64_t* __restrict__ opoff,
     const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z,
     int stage_doubles) {
@@ -372,7 +334,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1) patch_solve_bulk_kernel(
   double* ring = sbuf + size_t(NS * warp) * stage_doubles;
   uint64_t* bar = bars[warp];
   const int nw = gridDim.x * kBulkWarps;
-  const int p0 = pfirst + blockIdx.x * kBulkWarps + warp;   // patches [pfirst, npatch)
+  const int p0 = blockIdx.x * kBulkWarps + warp;
   if (lane == 0) {
 #pragma unroll
     for (int q = 0; q < NS; ++q) mbar_init(&bar[q], 1);
@@ -708,7 +670,7 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
         k, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkDynMax);                         \
     VK_CHECK_CUDA(attr);                                                                      \
     const int grid = std::min(want, vk_resident_blocks((const void*)k, kBulkWarps * 32, dsm)); \
-    le = vk_launch(k, dim3(grid), dim3(kBulkWarps * 32), dsm, vk_stream(stream), bytes, 0,    \
+    le = vk_launch(k, dim3(grid), dim3(kBulkWarps * 32), dsm, vk_stream(stream), bytes,       \
                    h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf,             \
                    stage_doubles);                                                            \
   } while (0)
@@ -792,124 +754,9 @@ extern "C" int vk_patches_accumulate(vk_patches_t h, double* out, double scale, 
   return VK_OK;
 }
 
-namespace {
-
-// percent of the patches in the first part of an overlapped sweep (0: off)
-int split_percent() {
-  static const int v = [] {
-    const char* e = getenv("VK_SWEEP_SPLIT");
-    return e ? atoi(e) : VK_SWEEP_SPLIT;
-  }();
-  return v;
-}
-
-int build_split(vk_patches_s* h, int pct) {
-  const int sp = static_cast<int>(int64_t(h->npatch) * pct / 100);
-  if (h->spl_list && h->spl_p == sp) return VK_OK;
-  cudaFree(h->spl_list);
-  h->spl_list = nullptr;
-  const int n = h->ndof;
-  std::vector<int32_t> dp(n + 1), ds(h->total);
-  VK_CHECK_CUDA(cudaMemcpy(dp.data(), h->dptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost));
-  if (h->total)
-    VK_CHECK_CUDA(cudaMemcpy(ds.data(), h->dslot, sizeof(int32_t) * h->total, cudaMemcpyDeviceToHost));
-  std::vector<int32_t> l1, l2;
-  for (int d = 0; d < n; ++d) {
-    int lastp = -1;
-    if (dp[d + 1] > dp[d]) {
-      const int64_t slot = ds[dp[d + 1] - 1];
-      lastp = static_cast<int>(std::upper_bound(h->h_off.begin(), h->h_off.end(), slot) -
-                               h->h_off.begin()) - 1;
-    }
-    (lastp < sp ? l1 : l2).push_back(d);
-  }
-  VK_CHECK_CUDA(cudaMalloc(&h->spl_list, sizeof(int32_t) * std::max(n, 1)));
-  if (!l1.empty())
-    VK_CHECK_CUDA(cudaMemcpy(h->spl_list, l1.data(), sizeof(int32_t) * l1.size(), cudaMemcpyHostToDevice));
-  if (!l2.empty())
-    VK_CHECK_CUDA(cudaMemcpy(h->spl_list + l1.size(), l2.data(), sizeof(int32_t) * l2.size(),
-                             cudaMemcpyHostToDevice));
-  h->spl_p = sp;
-  h->spl_n1 = static_cast<int>(l1.size());
-  h->spl_n2 = static_cast<int>(l2.size());
-  return VK_OK;
-}
-
-template <int MODE>
-cudaError_t launch_gather_list(const vk_patches_s* h, const int* list, int n, double* out,
-                               double scale, cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  const int grid = std::max(1, std::min((n + 255) / 256, 148 * 8));
-  return vk_launch(dof_gather_list_kernel<MODE>, dim3(grid), dim3(256), 0, st,
-                   12 * h->total + 16 * int64_t(n), n, list, (const int*)h->dptr,
-                   (const int*)h->dslot, (const double*)h->zbuf, out, scale);
-}
-
-cudaError_t gather_list(const vk_patches_s* h, const int* list, int n, double* out, double scale,
-                        int mode, cudaStream_t st) {
-  switch (mode) {
-    case VK_APPLY_OUT: return launch_gather_list<VK_APPLY_OUT>(h, list, n, out, scale, st);
-    case VK_APPLY_XSET: return launch_gather_list<VK_APPLY_XSET>(h, list, n, out, scale, st);
-    default: return launch_gather_list<VK_APPLY_XADD>(h, list, n, out, scale, st);
-  }
-}
-
-// K4a over patches [first, last) with the bulk kernel
-cudaError_t bulk_range(const vk_patches_s* h, const double* r, int first, int last, cudaStream_t st) {
-  const int rpl = (h->smax + 31) / 32;
-  const int stage_doubles = ((h->smax * h->smax + 1) & ~1);
-  const size_t dsm = bulk_smem(h->smax);
-  const int want = (last - first + kBulkWarps - 1) / kBulkWarps;
-  auto go = [&](auto k) -> cudaError_t {
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkDynMax);
-    if (attr != cudaSuccess) return attr;
-    const int grid = std::max(1, std::min(want, vk_resident_blocks((const void*)k, kBulkWarps * 32, dsm)));
-    return vk_launch(k, dim3(grid), dim3(kBulkWarps * 32), dsm, st, int64_t(1) << 62, first, last,
-                     (const int64_t*)h->off, (const int*)h->idx, (const double*)h->w,
-                     (const int64_t*)h->opoff, (const double*)h->inv, r, h->zbuf, stage_doubles);
-  };
-  return rpl <= 1 ? go(patch_solve_bulk_kernel<1>) : go(patch_solve_bulk_kernel<2>);
-}
-
-}  // namespace
-
 extern "C" int vk_patches_apply(vk_patches_t h, const double* r, double* out, double scale,
                                 int32_t mode, void* stream) {
   VK_REQUIRE(r && out, "vk_patches_apply: null argument");
-  const int pct = split_percent();
-  if (pct > 0 && pct < 100 && h && h->factored && h->npatch >= 148 * kBulkWarps * 8 &&
-      h->smax <= kBulkMaxS && !h->mixed_sizes && bulk_enabled() &&
-      bulk_smem(h->smax) <= size_t(kBulkDynMax)) {
-    // Overlapped sweep: the DoFs finished by the first part of the patch
-    // stream are summed on a side stream while the rest streams; the others
-    // after it.  Same per-DoF operations, disjoint outputs.
-    VK_REQUIRE(mode == VK_APPLY_OUT || mode == VK_APPLY_XSET || mode == VK_APPLY_XADD,
-               "vk_patches_apply: bad mode %d", mode);
-    if (int e = build_split(h, pct)) return e;
-    struct Side {
-      cudaStream_t s = nullptr;
-      cudaEvent_t a = nullptr, b = nullptr;
-      cudaError_t err = cudaSuccess;
-      Side() {
-        err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-        if (err == cudaSuccess) err = cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
-        if (err == cudaSuccess) err = cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
-      }
-    };
-    static Side side;
-    VK_CHECK_CUDA(side.err);
-    cudaStream_t st = vk_stream(stream);
-    VK_CHECK_CUDA(bulk_range(h, r, 0, h->spl_p, st));
-    VK_CHECK_CUDA(cudaEventRecord(side.a, st));
-    VK_CHECK_CUDA(bulk_range(h, r, h->spl_p, h->npatch, st));
-    VK_CHECK_CUDA(cudaStreamWaitEvent(side.s, side.a, 0));
-    VK_CHECK_CUDA(gather_list(h, h->spl_list, h->spl_n1, out, scale, mode, side.s));
-    VK_CHECK_CUDA(cudaEventRecord(side.b, side.s));
-    VK_CHECK_CUDA(gather_list(h, h->spl_list + h->spl_n1, h->spl_n2, out, scale, mode, st));
-    VK_CHECK_CUDA(cudaStreamWaitEvent(st, side.b, 0));
-    return VK_OK;
-  }
   if (int st = vk_patches_solve(h, r, stream)) return st;
   return vk_patches_accumulate(h, out, scale, mode, stream);
 }

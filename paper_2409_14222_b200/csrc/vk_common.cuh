@@ -75,11 +75,6 @@ struct Patches {
   int32_t* fac_ids = nullptr;
   int32_t* fac_status = nullptr;  // [npatch]
   std::vector<std::tuple<int, int, int>> fac_classes;
-  // overlapped sweep (vk_apply.cu): patches [0, spl_p) then [spl_p, npatch);
-  // DoFs whose last patch is < spl_p (list 1) can be summed while the second
-  // part streams, the others (list 2) after it
-  int spl_p = 0, spl_n1 = 0, spl_n2 = 0;
-  int32_t* spl_list = nullptr;  // [ndof]: list 1 then list 2
 };
 
 }  // namespace vk

@@ -233,7 +233,6 @@ void vk_patches_free(vk_patches_s* h) {
   cudaFree(h->zbuf);
   cudaFree(h->fac_ids);
   cudaFree(h->fac_status);
-  cudaFree(h->spl_list);
   delete h;
 }
 
