@@ -439,151 +439,6 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1) patch_solve_bulk_kernel(
   }
 }
 
-// Paired variant (VK_BULK_GROUP = GP > 1): groups of GP adjacent patches
-// are dealt round-robin to the warps (group q -> warp q mod nw), so at any
-// moment the warps read neighbouring operators (one sweep through HBM, as in
-// the bulk kernel) while each cp.async.bulk moves GP adjacent operators
-// (contiguous in the operator storage) at once.  Same per-element arithmetic.
-#ifndef VK_BULK_GROUP
-#define VK_BULK_GROUP 0
-#endif
-#ifndef VK_BULK_GSTAGES
-#define VK_BULK_GSTAGES 1
-#endif
-constexpr int kGroupP = VK_BULK_GROUP > 0 ? VK_BULK_GROUP : 1;
-constexpr int kGroupStages = VK_BULK_GSTAGES;
-inline size_t group_smem(int smax) {
-  return sizeof(double) * size_t((smax * smax + 1) & ~1) * kGroupP * kGroupStages * kBulkWarps;
-}
-
-template <int R>
-__global__ void __launch_bounds__(kBulkWarps * 32, 1) patch_solve_group_kernel(
-    int npatch, const int64_t* __restrict__ off, const int* __restrict__ idx,
-    const double* __restrict__ w, const int64_t* __restrict__ opoff,
-    const double* __restrict__ inv, const double* __restrict__ r, double* __restrict__ z,
-    int stage_doubles) {
-  constexpr int NS = kGroupStages;
-  constexpr int GP = kGroupP;
-  pdl_trigger();
-  extern __shared__ __align__(128) double sbuf[];   // [warps][NS][GP * stage_doubles]
-  __shared__ __align__(8) uint64_t bars[kBulkWarps][NS];
-  __shared__ double rsh_all[kBulkWarps][32 * R];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  double* rsh = rsh_all[warp];
-  const size_t gdoubles = size_t(GP) * stage_doubles;
-  double* ring = sbuf + size_t(NS * warp) * gdoubles;
-  uint64_t* bar = bars[warp];
-  const int nw = gridDim.x * kBulkWarps;
-  const int gw = blockIdx.x * kBulkWarps + warp;
-  if (lane == 0) {
-#pragma unroll
-    for (int q = 0; q < NS; ++q) mbar_init(&bar[q], 1);
-    mbar_fence_init();
-  }
-  __syncwarp();
-  const uint64_t pol = evict_first_policy();
-  // this warp's i-th patch: group g = i / GP (global group gw + g*nw), slot i % GP
-  auto pat = [&](int i) -> int {
-    const int64_t p = (int64_t(gw) + int64_t(i / GP) * nw) * GP + (i % GP);
-    return p < npatch ? static_cast<int>(p) : -1;
-  };
-  auto issue_group = [&](int g) {
-    const int64_t a = (int64_t(gw) + int64_t(g) * nw) * GP;
-    if (lane == 0 && a < npatch) {
-      const int b = static_cast<int>(a + GP < npatch ? a + GP : npatch);
-      const int64_t o0 = opoff[a], o1 = opoff[b];
-      const int st = g % NS;
-      const uint32_t bytes = static_cast<uint32_t>((o1 - o0) * sizeof(double));
-      mbar_expect_tx(&bar[st], bytes);
-      bulk_g2s(ring + size_t(st) * gdoubles, inv + o0, bytes, &bar[st], pol);
-    }
-  };
-#pragma unroll
-  for (int q = 0; q < NS; ++q) issue_group(q);
-
-  int64_t baseA = 0, baseB = 0, baseC = 0;
-  int sA = 0, sB = 0, sC = 0;
-  double rA[R];
-  int iB[R];
-  auto load_meta = [&](int p, int64_t& base, int& sz) {
-    if (p >= 0) {
-      base = off[p];
-      sz = static_cast<int>(off[p + 1] - base);
-    } else {
-      base = 0;
-      sz = 0;
-    }
-  };
-  load_meta(pat(0), baseA, sA);
-  pdl_wait();   // operators / structure above are setup data; r is not
-#pragma unroll
-  for (int q = 0; q < R; ++q) {
-    const int i = lane + 32 * q;
-    rA[q] = (i < sA) ? __ldg(r + idx[baseA + i]) : 0.0;
-  }
-  load_meta(pat(1), baseB, sB);
-#pragma unroll
-  for (int q = 0; q < R; ++q) {
-    const int i = lane + 32 * q;
-    iB[q] = (i < sB) ? idx[baseB + i] : 0;
-  }
-  load_meta(pat(2), baseC, sC);
-
-  uint32_t parity = 0u;
-  int64_t gbase_op = 0;
-  for (int i = 0;; ++i) {
-    const int p = pat(i);
-    if (p < 0) break;
-    const int g = i / GP, gi = i % GP, st = g % NS;
-    const int64_t base = baseA;
-    const int s = sA;
-#pragma unroll
-    for (int q = 0; q < R; ++q) rsh[lane + 32 * q] = rA[q];
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int ii = lane + 32 * q;
-      rA[q] = (ii < sB) ? __ldg(r + iB[q]) : 0.0;
-    }
-    baseA = baseB; sA = sB;
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int ii = lane + 32 * q;
-      iB[q] = (ii < sC) ? idx[baseC + ii] : 0;
-    }
-    baseB = baseC; sB = sC;
-    load_meta(pat(i + 3), baseC, sC);
-    const int64_t opp = opoff[p];
-    if (gi == 0) {
-      gbase_op = opp;
-      mbar_wait(&bar[st], (parity >> st) & 1u);
-      parity ^= (1u << st);
-    }
-    __syncwarp();
-    const double* A = ring + size_t(st) * gdoubles + (opp - gbase_op);
-    double y[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) y[q] = 0.0;
-#pragma unroll 4
-    for (int j = 0; j < s; ++j) {
-      const double rj = rsh[j];
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int ii = lane + 32 * q;
-        if (R == 1 || ii < s) y[q] = fma(A[j * s + ii], rj, y[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int ii = lane + 32 * q;
-      if (ii < s) z[base + ii] = __dmul_rn(__ldg(w + base + ii), y[q]);
-    }
-    __syncwarp();
-    const int pn = pat(i + 1);
-    if (gi == GP - 1 || pn < 0) issue_group(g + NS);   // group g fully read
-  }
-}
-
 // Chunked bulk-copy variant for s <= 128: a warp's patch operators are
 // streamed as a sequence of column chunks (cc columns, cc even,
 // cc*s*8 <= kChunkBytes; a patch's last chunk is padded to 16 bytes, which
@@ -802,25 +657,6 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
       default: VK_SPLIT(4); break;
     }
 #undef VK_SPLIT
-  } else if (VK_BULK_GROUP > 1 && h->npatch > 0 && h->smax <= kBulkMaxS && !h->mixed_sizes &&
-             bulk_enabled() && group_smem(h->smax) <= size_t(kBulkDynMax)) {
-    const int stage_doubles = ((h->smax * h->smax + 1) & ~1);
-    const size_t dsm = group_smem(h->smax);
-    const int want = (h->npatch + kBulkWarps - 1) / kBulkWarps;
-#define VK_GROUP(RV)                                                                          \
-  do {                                                                                        \
-    auto k = patch_solve_group_kernel<RV>;                                                    \
-    static const cudaError_t attr = cudaFuncSetAttribute(                                     \
-        k, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkDynMax);                         \
-    VK_CHECK_CUDA(attr);                                                                      \
-    const int grid = std::min(want, vk_resident_blocks((const void*)k, kBulkWarps * 32, dsm)); \
-    le = vk_launch(k, dim3(grid), dim3(kBulkWarps * 32), dsm, vk_stream(stream), bytes,       \
-                   h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf,             \
-                   stage_doubles);                                                            \
-  } while (0)
-    if (rpl <= 1) VK_GROUP(1);
-    else VK_GROUP(2);
-#undef VK_GROUP
   } else if (h->npatch > 0 && h->smax <= kBulkMaxS && !h->mixed_sizes && bulk_enabled() &&
              bulk_smem(h->smax) <= size_t(kBulkDynMax)) {
     // small patches: TMA bulk copies into a per-warp ring of kBulkStages
