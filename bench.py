@@ -287,8 +287,8 @@ def run_ours(args):
     h = ps.handle
 
     def step():
-        L.call("vk_patches_solve", h, L.ptr(r), sp)
-        L.call("vk_patches_accumulate", h, L.ptr(x), 0.5, L.VK_APPLY_XSET, sp)
+        L.call("vk_patches_solve", h, L.ptr(r), None, sp)
+        L.call("vk_patches_accumulate", h, None, L.ptr(x), 0.5, L.VK_APPLY_XSET, sp)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -313,9 +313,9 @@ def run_ours(args):
         for k in range(args.steps):
             a, b, c = ev[k]
             a.record(stream)
-            L.call("vk_patches_solve", h, L.ptr(r), sp)
+            L.call("vk_patches_solve", h, L.ptr(r), None, sp)
             b.record(stream)
-            L.call("vk_patches_accumulate", h, L.ptr(x), 0.5, L.VK_APPLY_XSET, sp)
+            L.call("vk_patches_accumulate", h, None, L.ptr(x), 0.5, L.VK_APPLY_XSET, sp)
             c.record(stream)
         torch.cuda.synchronize()
         ms_solve = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)

@@ -127,22 +127,34 @@ VK_API int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_host, i
 VK_API int vk_patches_export_inverse(vk_patches_t h, int32_t first, int32_t count, double* inv_host);
 /* additive sweep (vanka.apply_additive, vanka.py:142-148, + mg.py:268-271):
  * mode VK_APPLY_OUT: out = sum_i R_i^T W_i A_i^{-1} R_i r ; XSET/XADD: see above.
- * Deterministic: contributions summed per DoF in patch order. */
+ * Deterministic: contributions summed per DoF in patch order.
+ * zbuf: DEVICE buffer of `total` doubles (vk_patches_info) for the weighted
+ * local corrections, or NULL for the handle's own.  The handle is immutable
+ * after factor, so sweeps of one handle may run concurrently on different
+ * streams as long as each passes its own zbuf (and its own out). */
 VK_API int vk_patches_apply(vk_patches_t h, const double* r, double* out, double scale,
-                     int32_t mode, void* stream);
+                     int32_t mode, double* zbuf, void* stream);
 /* the two halves of vk_patches_apply, for per-kernel timing:
- * solve: z = W A_i^{-1} R_i r into the handle's sum(s) buffer (K4a);
+ * solve: z = W A_i^{-1} R_i r into zbuf (NULL = handle's; K4a);
  * accumulate: per-DoF patch-ordered sum of z + epilogue (K4b). */
-VK_API int vk_patches_solve(vk_patches_t h, const double* r, void* stream);
-VK_API int vk_patches_accumulate(vk_patches_t h, double* out, double scale, int32_t mode,
-                                 void* stream);
+VK_API int vk_patches_solve(vk_patches_t h, const double* r, double* zbuf, void* stream);
+VK_API int vk_patches_accumulate(vk_patches_t h, const double* zbuf, double* out, double scale,
+                                 int32_t mode, void* stream);
 VK_API int vk_patches_destroy(vk_patches_t h);
 
 /* ---------------- dense / vector helpers (FGMRES + V-cycle plumbing) -------
  * sparsela.fgmres (sparsela.py:117-191), coarse_solve (mg.py:274-279),
- * v_cycle bc copy (mg.py:298-300).  Device scalars are single doubles. */
+ * v_cycle bc copy (mg.py:298-300).  Device scalars are single doubles.
+ *
+ * Reductions take a caller-owned DEVICE scratch of VK_REDUCE_SCRATCH doubles,
+ * zero-filled once before its first use (each reduction leaves it ready for
+ * the next).  Reductions in flight at the same time (different streams) need
+ * distinct scratch buffers; one buffer may serve any number of reductions
+ * ordered on one stream (or one CUDA graph). */
+#define VK_REDUCE_SCRATCH 320
 /* *out_dev = x . y  (deterministic two-level reduction, one launch) */
-VK_API int vk_dot(int64_t n, const double* x, const double* y, double* out_dev, void* stream);
+VK_API int vk_dot(int64_t n, const double* x, const double* y, double* out_dev,
+                  double* scratch_dev, void* stream);
 /* y = y - (*a_dev) * x */
 VK_API int vk_axpy_dev(int64_t n, const double* a_dev, const double* x, double* y, void* stream);
 /* Fused modified-Gram-Schmidt step (sparsela.py:160-163): y = y - (*a_dev) * x,
@@ -150,14 +162,16 @@ VK_API int vk_axpy_dev(int64_t n, const double* a_dev, const double* x, double* 
  * uses vk_dot's thread/element mapping and reduction tree, so the result is
  * bit-identical to vk_axpy_dev followed by vk_dot / vk_nrm2. */
 VK_API int vk_axpy_dot(int64_t n, const double* a_dev, const double* x, double* y, const double* x2,
-                       double* out_dev, int32_t sqrt_out, void* stream);
+                       double* out_dev, int32_t sqrt_out, double* scratch_dev, void* stream);
 /* y = y + a * x  (host scalar) */
 VK_API int vk_axpy(int64_t n, double a, const double* x, double* y, void* stream);
 /* y = x / (*d_dev) */
 VK_API int vk_div_dev(int64_t n, const double* x, const double* d_dev, double* y, void* stream);
 /* *out_dev = sqrt(x . x) */
-VK_API int vk_nrm2(int64_t n, const double* x, double* out_dev, void* stream);
-/* x = x - q (q . x) in place (NullspaceProjector, sparsela.py:113-114) */
+VK_API int vk_nrm2(int64_t n, const double* x, double* out_dev, double* scratch_dev,
+                   void* stream);
+/* x = x - q (q . x) in place (NullspaceProjector, sparsela.py:113-114);
+ * scratch_dev: VK_REDUCE_SCRATCH doubles as above */
 VK_API int vk_project(int64_t n, const double* q, double* x, double* scratch_dev, void* stream);
 /* dst[idx[k]] = src[idx[k]] */
 VK_API int vk_copy_index(int64_t m, const int32_t* idx, const double* src, double* dst, void* stream);

@@ -21,6 +21,7 @@ VK_ERR_ARG, VK_ERR_CUDA, VK_ERR_ALLOC, VK_ERR_UNSUPPORTED = -1, -2, -3, -4
 VK_PATCH_OK, VK_PATCH_ZERO_ROW, VK_PATCH_SMALL_PIVOT = 0, 1, 2
 VK_WEIGHT_INVMULT, VK_WEIGHT_UNIT = 0, 1
 VK_APPLY_OUT, VK_APPLY_XSET, VK_APPLY_XADD = 0, 1, 2
+VK_REDUCE_SCRATCH = 320          # doubles of caller-owned reduction scratch
 
 _p = C.c_void_p
 _i32, _i64, _f64 = C.c_int32, C.c_int64, C.c_double
@@ -46,16 +47,16 @@ SIGNATURES = {
     "vk_patches_extract": (C.c_int, [_p, _p, _i32, _i32, _p]),
     "vk_patches_factor": (C.c_int, [_p, _p, _p, _P_i32]),
     "vk_patches_export_inverse": (C.c_int, [_p, _i32, _i32, _p]),
-    "vk_patches_apply": (C.c_int, [_p, _p, _p, _f64, _i32, _p]),
-    "vk_patches_solve": (C.c_int, [_p, _p, _p]),
-    "vk_patches_accumulate": (C.c_int, [_p, _p, _f64, _i32, _p]),
+    "vk_patches_apply": (C.c_int, [_p, _p, _p, _f64, _i32, _p, _p]),
+    "vk_patches_solve": (C.c_int, [_p, _p, _p, _p]),
+    "vk_patches_accumulate": (C.c_int, [_p, _p, _p, _f64, _i32, _p]),
     "vk_patches_destroy": (C.c_int, [_p]),
-    "vk_dot": (C.c_int, [_i64, _p, _p, _p, _p]),
+    "vk_dot": (C.c_int, [_i64, _p, _p, _p, _p, _p]),
     "vk_axpy_dev": (C.c_int, [_i64, _p, _p, _p, _p]),
-    "vk_axpy_dot": (C.c_int, [_i64, _p, _p, _p, _p, _p, _i32, _p]),
+    "vk_axpy_dot": (C.c_int, [_i64, _p, _p, _p, _p, _p, _i32, _p, _p]),
     "vk_axpy": (C.c_int, [_i64, _f64, _p, _p, _p]),
     "vk_div_dev": (C.c_int, [_i64, _p, _p, _p, _p]),
-    "vk_nrm2": (C.c_int, [_i64, _p, _p, _p]),
+    "vk_nrm2": (C.c_int, [_i64, _p, _p, _p, _p]),
     "vk_project": (C.c_int, [_i64, _p, _p, _p, _p]),
     "vk_copy_index": (C.c_int, [_i64, _p, _p, _p, _p]),
     "vk_gemv": (C.c_int, [_i32, _i32, _p, _p, _p, _p]),
@@ -127,6 +128,13 @@ def stream_ptr(stream=None):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+def reduce_scratch(count: int = 1):
+    """Zero-filled device scratch for ``count`` independent reduction
+    streams (``VK_REDUCE_SCRATCH`` doubles each); row k serves stream k."""
+    import torch
+    return torch.zeros((count, VK_REDUCE_SCRATCH), dtype=torch.float64, device="cuda")
 
 
 def require_cuda():

@@ -202,11 +202,12 @@ __global__ void __launch_bounds__(256) dof_gather_kernel(int ndof, const int* __
 }
 
 template <int MODE>
-cudaError_t launch_gather(const vk_patches_s* h, double* out, double scale, cudaStream_t st) {
+cudaError_t launch_gather(const vk_patches_s* h, const double* zbuf, double* out, double scale,
+                          cudaStream_t st) {
   const int grid = std::max(1, std::min((h->ndof + 255) / 256, 148 * 8));
   return vk_launch(dof_gather_kernel<MODE>, dim3(grid), dim3(256), 0, st,
                    12 * h->total + 16 * int64_t(h->ndof), h->ndof, (const int*)h->dptr,
-                   (const int*)h->dslot, (const double*)h->zbuf, out, scale);
+                   (const int*)h->dslot, zbuf, out, scale);
 }
 
 }  // namespace
@@ -423,7 +424,7 @@ __global__ void __launch_bounds__(kBulkWarps * 32, 1) patch_solve_bulk_kernel(
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         const int i = lane + 32 * q;
-        if (R == 1 || i < s) y[q] = fma(A[j * s + i], rj, y[q]);
+        if (i < s) y[q] = fma(A[j * s + i], rj, y[q]);   // lanes past s stay in their stage
       }
     }
 #pragma unroll
@@ -636,9 +637,10 @@ static bool chunk_enabled() {
   return v;
 }
 
-extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
+extern "C" int vk_patches_solve(vk_patches_t h, const double* r, double* zbuf, void* stream) {
   if (int st = check_apply(h)) return st;
   VK_REQUIRE(r, "vk_patches_solve: null residual");
+  double* const z = zbuf ? zbuf : h->zbuf;  // caller-owned z: concurrent applies
   const int rpl = (h->smax + 31) / 32;
   const int64_t bytes = 8 * h->inv_total + 20 * h->total;   // for the PDL decision
   cudaError_t le = cudaSuccess;
@@ -649,7 +651,7 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
 #define VK_SPLIT(RV)                                                                        \
   le = vk_launch(patch_solve_split_kernel<RV, G>, dim3(grid), dim3(kApplyWarps * 32), 0,    \
                  vk_stream(stream), bytes, h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, \
-                 r, h->zbuf)
+                 r, z)
     switch (rpl) {
       case 1: VK_SPLIT(1); break;
       case 2: VK_SPLIT(2); break;
@@ -666,12 +668,10 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
 #define VK_BULK(RV)                                                                           \
   do {                                                                                        \
     auto k = patch_solve_bulk_kernel<RV>;                                                     \
-    static const cudaError_t attr = cudaFuncSetAttribute(                                     \
-        k, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkDynMax);                         \
-    VK_CHECK_CUDA(attr);                                                                      \
+    VK_CHECK_CUDA(vk_smem_optin((const void*)k, kBulkDynMax));                                \
     const int grid = std::min(want, vk_resident_blocks((const void*)k, kBulkWarps * 32, dsm)); \
     le = vk_launch(k, dim3(grid), dim3(kBulkWarps * 32), dsm, vk_stream(stream), bytes,       \
-                   h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf,             \
+                   h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, z,             \
                    stage_doubles);                                                            \
   } while (0)
     if (rpl <= 1) VK_BULK(1);
@@ -684,12 +684,10 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
 #define VK_CHUNK(RV)                                                                          \
   do {                                                                                        \
     auto k = patch_solve_chunk_kernel<RV>;                                                    \
-    static const cudaError_t attr = cudaFuncSetAttribute(                                     \
-        k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));                            \
-    VK_CHECK_CUDA(attr);                                                                      \
+    VK_CHECK_CUDA(vk_smem_optin((const void*)k, int(dsm)));                                   \
     const int grid = std::min(want, vk_resident_blocks((const void*)k, kApplyWarps * 32, dsm)); \
     le = vk_launch(k, dim3(grid), dim3(kApplyWarps * 32), dsm, vk_stream(stream), bytes,      \
-                   h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf);            \
+                   h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, z);            \
   } while (0)
     switch (rpl) {
       case 1: VK_CHUNK(1); break;
@@ -706,12 +704,12 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
     auto k = patch_solve_kernel<RV, true>;                                                  \
     const int grid = std::min(want, vk_resident_blocks((const void*)k, kApplyWarps * 32));  \
     k<<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(                                    \
-        h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf);                     \
+        h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, z);                     \
   } else {                                                                                  \
     auto k = patch_solve_kernel<RV, false>;                                                 \
     const int grid = std::min(want, vk_resident_blocks((const void*)k, kApplyWarps * 32));  \
     k<<<grid, kApplyWarps * 32, 0, vk_stream(stream)>>>(                                    \
-        h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, h->zbuf);                     \
+        h->npatch, h->off, h->idx, h->w, h->opoff, h->inv, r, z);                     \
   }
     switch (rpl) {
       case 1: VK_SOLVE(1); break;
@@ -731,9 +729,10 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, void* stream) {
   return VK_OK;
 }
 
-extern "C" int vk_patches_accumulate(vk_patches_t h, double* out, double scale, int32_t mode,
-                                     void* stream) {
+extern "C" int vk_patches_accumulate(vk_patches_t h, const double* zbuf, double* out,
+                                     double scale, int32_t mode, void* stream) {
   if (int st = check_apply(h)) return st;
+  const double* const z = zbuf ? zbuf : h->zbuf;
   VK_REQUIRE(out, "vk_patches_accumulate: null output");
   VK_REQUIRE(mode == VK_APPLY_OUT || mode == VK_APPLY_XSET || mode == VK_APPLY_XADD,
              "vk_patches_apply: bad mode %d", mode);
@@ -741,9 +740,9 @@ extern "C" int vk_patches_accumulate(vk_patches_t h, double* out, double scale, 
   if (h->ndof > 0) {
     cudaError_t e;
     switch (mode) {
-      case VK_APPLY_OUT: e = launch_gather<VK_APPLY_OUT>(h, out, scale, st); break;
-      case VK_APPLY_XSET: e = launch_gather<VK_APPLY_XSET>(h, out, scale, st); break;
-      default: e = launch_gather<VK_APPLY_XADD>(h, out, scale, st); break;
+      case VK_APPLY_OUT: e = launch_gather<VK_APPLY_OUT>(h, z, out, scale, st); break;
+      case VK_APPLY_XSET: e = launch_gather<VK_APPLY_XSET>(h, z, out, scale, st); break;
+      default: e = launch_gather<VK_APPLY_XADD>(h, z, out, scale, st); break;
     }
     if (e != cudaSuccess) {
       vk::set_error("vk_patches_accumulate: %s", cudaGetErrorString(e));
@@ -755,8 +754,8 @@ extern "C" int vk_patches_accumulate(vk_patches_t h, double* out, double scale, 
 }
 
 extern "C" int vk_patches_apply(vk_patches_t h, const double* r, double* out, double scale,
-                                int32_t mode, void* stream) {
+                                int32_t mode, double* zbuf, void* stream) {
   VK_REQUIRE(r && out, "vk_patches_apply: null argument");
-  if (int st = vk_patches_solve(h, r, stream)) return st;
-  return vk_patches_accumulate(h, out, scale, mode, stream);
+  if (int st = vk_patches_solve(h, r, zbuf, stream)) return st;
+  return vk_patches_accumulate(h, zbuf, out, scale, mode, stream);
 }

@@ -4,7 +4,10 @@
 // mg.py:298-300).  Reductions are deterministic: fixed grid, fixed
 // per-thread order, tree in shared memory, last-arriving block combines the
 // block partials in index order (one launch, graph-capturable; the arrival
-// counter resets itself).
+// counter resets itself).  The block partials and the arrival counter live in
+// a caller-owned scratch buffer (VK_REDUCE_SCRATCH doubles, zero-filled once):
+// reductions in flight on different streams never share state, so the calls
+// are re-entrant across streams as the header promises.
 #include <algorithm>
 
 #include "vk_common.cuh"
@@ -14,8 +17,43 @@ namespace {
 constexpr int kRedBlock = 256;
 constexpr int kRedGrid = 296;
 
-__device__ double g_partials[kRedGrid];
-__device__ unsigned int g_arrive = 0;
+static_assert(kRedGrid + 2 <= VK_REDUCE_SCRATCH, "scratch too small");
+
+// scratch layout: [0, kRedGrid) block partials, [kRedGrid] arrival counter
+// (as an unsigned int), [kRedGrid + 1] a spare scalar (vk_project's q.x)
+__device__ __forceinline__ unsigned int* arrive_of(double* scratch) {
+  return reinterpret_cast<unsigned int*>(scratch + kRedGrid);
+}
+
+// last-arriving block combines the partials in block order
+__device__ __forceinline__ void grid_finish(double bs, double* sh, double* scratch, double* out,
+                                            bool fin_sqrt) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    scratch[blockIdx.x] = bs;
+    __threadfence();
+    const unsigned int ticket = atomicAdd(arrive_of(scratch), 1u);
+    last = (ticket == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double v = 0.0;
+    for (int b = threadIdx.x; b < gridDim.x; b += kRedBlock)
+      v = __dadd_rn(v, *((volatile double*)&scratch[b]));
+    __syncthreads();
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = kRedBlock / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + o]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      *out = fin_sqrt ? sqrt(sh[0]) : sh[0];
+      *arrive_of(scratch) = 0u;
+    }
+  }
+}
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
   const int t = threadIdx.x;
@@ -32,33 +70,17 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 template <int FIN>
 __global__ void __launch_bounds__(kRedBlock) dot_kernel(int64_t n, const double* __restrict__ x,
                                                         const double* __restrict__ y,
-                                                        double* __restrict__ out) {
+                                                        double* __restrict__ out,
+                                                        double* scratch) {
   pdl_trigger();
   pdl_wait();
   __shared__ double sh[kRedBlock];
-  __shared__ bool last;
   double acc = 0.0;
   for (int64_t i = blockIdx.x * int64_t(kRedBlock) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * kRedBlock)
     acc = fma(x[i], y[i], acc);
   const double bs = block_sum(acc, sh);
-  if (threadIdx.x == 0) {
-    g_partials[blockIdx.x] = bs;
-    __threadfence();
-    const unsigned int ticket = atomicAdd(&g_arrive, 1u);
-    last = (ticket == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    double v = 0.0;
-    for (int b = threadIdx.x; b < gridDim.x; b += kRedBlock) v = __dadd_rn(v, *((volatile double*)&g_partials[b]));
-    const double tot = block_sum(v, sh);
-    if (threadIdx.x == 0) {
-      *out = FIN ? sqrt(tot) : tot;
-      g_arrive = 0;
-    }
-  }
+  grid_finish(bs, sh, scratch, out, FIN != 0);
 }
 
 // y -= a x, then the dot of x2 with the updated y: element i is owned by the
@@ -68,11 +90,11 @@ template <int FIN>
 __global__ void __launch_bounds__(kRedBlock) axpy_dot_kernel(int64_t n, const double* __restrict__ a,
                                                              const double* __restrict__ x,
                                                              double* y, const double* x2,
-                                                             double* __restrict__ out) {
+                                                             double* __restrict__ out,
+                                                             double* scratch) {
   pdl_trigger();
   pdl_wait();
   __shared__ double sh[kRedBlock];
-  __shared__ bool last;
   const double av = *a;
   double acc = 0.0;
   for (int64_t i = blockIdx.x * int64_t(kRedBlock) + threadIdx.x; i < n;
@@ -82,23 +104,7 @@ __global__ void __launch_bounds__(kRedBlock) axpy_dot_kernel(int64_t n, const do
     acc = fma(x2 == y ? yn : x2[i], yn, acc);
   }
   const double bs = block_sum(acc, sh);
-  if (threadIdx.x == 0) {
-    g_partials[blockIdx.x] = bs;
-    __threadfence();
-    const unsigned int ticket = atomicAdd(&g_arrive, 1u);
-    last = (ticket == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    double v = 0.0;
-    for (int b = threadIdx.x; b < gridDim.x; b += kRedBlock) v = __dadd_rn(v, *((volatile double*)&g_partials[b]));
-    const double tot = block_sum(v, sh);
-    if (threadIdx.x == 0) {
-      *out = FIN ? sqrt(tot) : tot;
-      g_arrive = 0;
-    }
-  }
+  grid_finish(bs, sh, scratch, out, FIN != 0);
 }
 
 __global__ void axpy_dev_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ x,
@@ -189,16 +195,18 @@ __global__ void project_apply_kernel(int64_t n, const double* __restrict__ q, co
 
 #define VK_VEC_GRID(n) vk_grid((n), 256, 148 * 8)
 
-extern "C" int vk_dot(int64_t n, const double* x, const double* y, double* out_dev, void* stream) {
-  VK_REQUIRE(out_dev && n >= 0 && (n == 0 || (x && y)), "vk_dot: bad argument");
-  VK_CHECK_CUDA(vk_launch(dot_kernel<0>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 16 * n, n, x, y, out_dev));
+extern "C" int vk_dot(int64_t n, const double* x, const double* y, double* out_dev,
+                      double* scratch_dev, void* stream) {
+  VK_REQUIRE(out_dev && scratch_dev && n >= 0 && (n == 0 || (x && y)), "vk_dot: bad argument");
+  VK_CHECK_CUDA(vk_launch(dot_kernel<0>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 16 * n, n, x, y, out_dev, scratch_dev));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
 
-extern "C" int vk_nrm2(int64_t n, const double* x, double* out_dev, void* stream) {
-  VK_REQUIRE(out_dev && n >= 0 && (n == 0 || x), "vk_nrm2: bad argument");
-  VK_CHECK_CUDA(vk_launch(dot_kernel<1>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 8 * n, n, x, x, out_dev));
+extern "C" int vk_nrm2(int64_t n, const double* x, double* out_dev, double* scratch_dev,
+                       void* stream) {
+  VK_REQUIRE(out_dev && scratch_dev && n >= 0 && (n == 0 || x), "vk_nrm2: bad argument");
+  VK_CHECK_CUDA(vk_launch(dot_kernel<1>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 8 * n, n, x, x, out_dev, scratch_dev));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
@@ -212,12 +220,13 @@ extern "C" int vk_axpy_dev(int64_t n, const double* a_dev, const double* x, doub
 }
 
 extern "C" int vk_axpy_dot(int64_t n, const double* a_dev, const double* x, double* y, const double* x2,
-                           double* out_dev, int32_t sqrt_out, void* stream) {
-  VK_REQUIRE(a_dev && out_dev && n >= 0 && (n == 0 || (x && y && x2)), "vk_axpy_dot: bad argument");
+                           double* out_dev, int32_t sqrt_out, double* scratch_dev, void* stream) {
+  VK_REQUIRE(a_dev && out_dev && scratch_dev && n >= 0 && (n == 0 || (x && y && x2)),
+             "vk_axpy_dot: bad argument");
   if (sqrt_out)
-    VK_CHECK_CUDA(vk_launch(axpy_dot_kernel<1>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 8 * n, n, a_dev, x, y, x2, out_dev));
+    VK_CHECK_CUDA(vk_launch(axpy_dot_kernel<1>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 8 * n, n, a_dev, x, y, x2, out_dev, scratch_dev));
   else
-    VK_CHECK_CUDA(vk_launch(axpy_dot_kernel<0>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 16 * n, n, a_dev, x, y, x2, out_dev));
+    VK_CHECK_CUDA(vk_launch(axpy_dot_kernel<0>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 16 * n, n, a_dev, x, y, x2, out_dev, scratch_dev));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
@@ -241,8 +250,9 @@ extern "C" int vk_div_dev(int64_t n, const double* x, const double* d_dev, doubl
 extern "C" int vk_project(int64_t n, const double* q, double* x, double* scratch_dev, void* stream) {
   VK_REQUIRE(q && x && scratch_dev, "vk_project: null argument");
   if (n == 0) return VK_OK;
-  VK_CHECK_CUDA(vk_launch(dot_kernel<0>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 16 * n, n, q, x, scratch_dev));
-  VK_CHECK_CUDA(vk_launch(project_apply_kernel, dim3(VK_VEC_GRID(n)), dim3(256), 0, vk_stream(stream), 24 * n, n, q, scratch_dev, x));
+  double* qx = scratch_dev + kRedGrid + 1;
+  VK_CHECK_CUDA(vk_launch(dot_kernel<0>, dim3(kRedGrid), dim3(kRedBlock), 0, vk_stream(stream), 16 * n, n, q, x, qx, scratch_dev));
+  VK_CHECK_CUDA(vk_launch(project_apply_kernel, dim3(VK_VEC_GRID(n)), dim3(256), 0, vk_stream(stream), 24 * n, n, q, (const double*)qx, x));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }

@@ -123,15 +123,21 @@ static inline int vk_grid(int64_t work, int block, int cap = 148 * 16) {
 // x occupancy), cached per (kernel, block size, dynamic shared memory).
 // Persistent grid-stride kernels launch exactly this many so there is no
 // partial last wave.
+static inline int vk_current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
 static inline int vk_resident_blocks(const void* kernel, int block, size_t smem = 0) {
   static std::mutex mu;
-  static std::map<std::tuple<const void*, int, size_t>, int> cache;
+  static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
   std::lock_guard<std::mutex> lock(mu);
-  const auto key = std::make_tuple(kernel, block, smem);
+  const int dev = vk_current_device();   // occupancy is cached per device
+  const auto key = std::make_tuple(kernel, block, smem, dev);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
+  int sms = 148, per_sm = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess ||
       per_sm < 1)
@@ -139,6 +145,22 @@ static inline int vk_resident_blocks(const void* kernel, int block, size_t smem 
   const int n = per_sm * sms;
   cache.emplace(key, n);
   return n;
+}
+
+// Opt `kernel` into `bytes` of dynamic shared memory on the CURRENT device
+// (a function attribute is per device: a process driving a second GPU must
+// set it there too).  Done once per (kernel, device, bytes).
+static inline cudaError_t vk_smem_optin(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int>, int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(kernel, vk_current_device());
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[key] = bytes;
+  return e;
 }
 
 // TMA 1-D bulk copies (cp.async.bulk) completed on an mbarrier.

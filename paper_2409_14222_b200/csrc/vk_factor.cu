@@ -556,7 +556,7 @@ int launch_class(int smax, const int* d_ids, int count, const vk_patches_s* h, c
   do {                                                                                         \
     auto kern = factor_tile_kernel<TR_, TC_, RA_, CB_, MB_>;                                      \
     const size_t dsm = sizeof(double) * size_t(TR_ * RA_) * size_t((TR_ * RA_) | 1);          \
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));    \
+    e = vk_smem_optin((const void*)kern, int(dsm));                                            \
     int per_sm = 1;                                                                            \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TR_ * TC_, dsm);              \
     const int grid = std::max(1, std::min(count, 148 * std::max(per_sm, 1)));                 \
@@ -583,20 +583,17 @@ int launch_class(int smax, const int* d_ids, int count, const vk_patches_s* h, c
       return VK_ERR_CUDA;
     }
   } else if (smax <= 32) {
-    VK_CHECK_CUDA(cudaFuncSetAttribute(factor_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(smem)));
+    VK_CHECK_CUDA(vk_smem_optin((const void*)factor_kernel<128>, int(smem)));
     factor_kernel<128><<<std::min(count, 148 * 32), 128, smem, st>>>(
         d_ids, count, h->off, h->idx, a->indptr, a->indices, a->data, h->opoff, h->inv, d_status,
         blocks, d_boff, extract_only);
   } else if (smax <= 64) {
-    VK_CHECK_CUDA(cudaFuncSetAttribute(factor_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(smem)));
+    VK_CHECK_CUDA(vk_smem_optin((const void*)factor_kernel<256>, int(smem)));
     factor_kernel<256><<<std::min(count, 148 * 16), 256, smem, st>>>(
         d_ids, count, h->off, h->idx, a->indptr, a->indices, a->data, h->opoff, h->inv, d_status,
         blocks, d_boff, extract_only);
   } else {
-    VK_CHECK_CUDA(cudaFuncSetAttribute(factor_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(smem)));
+    VK_CHECK_CUDA(vk_smem_optin((const void*)factor_kernel<512>, int(smem)));
     factor_kernel<512><<<std::min(count, 148 * 8), 512, smem, st>>>(
         d_ids, count, h->off, h->idx, a->indptr, a->indices, a->data, h->opoff, h->inv, d_status,
         blocks, d_boff, extract_only);
@@ -734,7 +731,7 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
   int* d_status = h->fac_status;
   // The largest class (most work) runs on the legacy stream, the small ones
   // (boundary / coarse patches) beside it on an auxiliary stream; one join.
-  struct AuxStream {                 // created once, thread-safe (function-local static)
+  struct AuxStream {                 // one per device (streams belong to a device)
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     cudaError_t err = cudaSuccess;
@@ -744,7 +741,16 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
       if (err == cudaSuccess) err = cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
     }
   };
-  static AuxStream aux_streams;
+  static std::mutex aux_mu;
+  static std::map<int, AuxStream*> aux_by_dev;
+  AuxStream* aux_p;
+  {
+    std::lock_guard<std::mutex> lock(aux_mu);
+    AuxStream*& slot = aux_by_dev[vk_current_device()];
+    if (!slot) slot = new AuxStream();
+    aux_p = slot;
+  }
+  AuxStream& aux_streams = *aux_p;
   VK_CHECK_CUDA(aux_streams.err);
   cudaStream_t aux = aux_streams.s;
   cudaEvent_t ev_fork = aux_streams.fork, ev_join = aux_streams.join;

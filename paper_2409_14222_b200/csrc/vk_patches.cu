@@ -393,45 +393,60 @@ extern "C" int vk_patches_from_lists(const int64_t* offsets, const int32_t* indi
                                      int32_t npatch, int32_t ndof, vk_patches_t* out) {
   VK_REQUIRE(out && offsets && num_velocity && npatch >= 0 && ndof >= 0,
              "vk_patches_from_lists: bad argument");
+  for (int p = 0; p < npatch; ++p)
+    VK_REQUIRE(offsets[p + 1] >= offsets[p], "vk_patches_from_lists: offsets must be nondecreasing");
+  const int64_t in_total = offsets[npatch] - offsets[0];
+  VK_REQUIRE(in_total == 0 || indices, "vk_patches_from_lists: null indices");
+  // size-0 patches contribute nothing to the sweep and have no block to
+  // factor: they are dropped like the reference's _finish drops empty
+  // patches (vanka.py:64-65); cand_of_patch maps kept -> input position
+  std::vector<int32_t> cand, nv;
+  std::vector<int64_t> koff(1, 0);
+  std::vector<int32_t> hi;
+  std::vector<double> kw;
+  hi.reserve(in_total);
+  for (int p = 0; p < npatch; ++p) {
+    const int64_t a = offsets[p], b = offsets[p + 1];
+    if (b == a) continue;
+    cand.push_back(p);
+    nv.push_back(num_velocity[p]);
+    hi.insert(hi.end(), indices + (a - offsets[0]), indices + (b - offsets[0]));
+    if (weights) kw.insert(kw.end(), weights + (a - offsets[0]), weights + (b - offsets[0]));
+    koff.push_back(koff.back() + (b - a));
+  }
   auto* h = new vk_patches_s();
   h->ndof = ndof;
-  h->npatch = npatch;
+  h->npatch = static_cast<int32_t>(cand.size());
   h->weighting = weights ? VK_WEIGHT_INVMULT : VK_WEIGHT_UNIT;
-  h->h_off.assign(offsets, offsets + npatch + 1);
-  h->total = h->h_off[npatch];
+  h->h_off = koff;
+  h->total = koff.back();
   int smax = 0;
-  for (int p = 0; p < npatch; ++p) {
-    const int64_t s = h->h_off[p + 1] - h->h_off[p];
-    if (s < 0) {
-      vk_patches_free(h);
-      vk::set_error("vk_patches_from_lists: offsets must be nondecreasing");
-      return VK_ERR_ARG;
-    }
-    smax = std::max<int>(smax, static_cast<int>(s));
-  }
+  for (int p = 0; p < h->npatch; ++p)
+    smax = std::max<int>(smax, static_cast<int>(koff[p + 1] - koff[p]));
   h->smax = smax;
-  std::vector<int32_t> hi(indices, indices + h->total);
   for (int64_t k = 0; k < h->total; ++k)
     if (hi[k] < 0 || hi[k] >= ndof) {
       vk_patches_free(h);
       vk::set_error("vk_patches_from_lists: index %d out of range", hi[k]);
       return VK_ERR_ARG;
     }
-  for (int p = 0; p < npatch; ++p)
-    for (int64_t k = h->h_off[p] + 1; k < h->h_off[p + 1]; ++k)
+  for (int p = 0; p < h->npatch; ++p)
+    for (int64_t k = koff[p] + 1; k < koff[p + 1]; ++k)
       if (hi[k - 1] >= hi[k]) {
         vk_patches_free(h);
-        vk::set_error("vk_patches_from_lists: patch %d indices must be sorted and duplicate-free", p);
+        vk::set_error("vk_patches_from_lists: patch %d indices must be sorted and duplicate-free",
+                      cand[p]);
         return VK_ERR_ARG;
       }
+  npatch = h->npatch;
+  const int32_t* num_velocity_k = nv.data();
+  const double* weights_k = weights ? kw.data() : nullptr;
   std::vector<double> hw;
-  if (!weights) hw.assign(std::max<int64_t>(h->total, 1), 1.0);
-  std::vector<int32_t> cand(npatch);
-  for (int p = 0; p < npatch; ++p) cand[p] = p;
+  if (!weights_k) hw.assign(std::max<int64_t>(h->total, 1), 1.0);
   int st = upload(&h->off, h->h_off.data(), npatch + 1);
   if (!st) st = upload(&h->idx, hi.data(), h->total);
-  if (!st) st = upload(&h->nvel, num_velocity, npatch);
-  if (!st) st = upload(&h->w, weights ? weights : hw.data(), h->total);
+  if (!st) st = upload(&h->nvel, num_velocity_k, npatch);
+  if (!st) st = upload(&h->w, weights_k ? weights_k : hw.data(), h->total);
   if (!st) st = upload(&h->cand, cand.data(), npatch);
   if (st) {
     vk_patches_free(h);

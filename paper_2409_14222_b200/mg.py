@@ -125,7 +125,7 @@ class MgHierarchy:
         self.coarse_inverse = torch.linalg.inv(m).contiguous()          # mg.py:232
         self.coarse_factor = self.coarse_inverse
         self.q = q
-        self._scratch = torch.zeros(4, dtype=torch.float64, device="cuda")
+        self._scratch = L.reduce_scratch()[0]     # this hierarchy's reductions
         self._graphs = {}
         self._in = torch.zeros(levels[-1].n, dtype=torch.float64, device="cuda")
 
@@ -146,7 +146,7 @@ class MgHierarchy:
         c.r.copy_(rhs)
         L.call("vk_project", n, L.ptr(self.q), L.ptr(c.r), L.ptr(self._scratch), st)
         L.call("vk_gemv", n, n, L.ptr(self.coarse_inverse), L.ptr(c.r), L.ptr(x), st)
-        L.call("vk_project", n, L.ptr(self.q), L.ptr(x), L.ptr(self._scratch[1:]), st)
+        L.call("vk_project", n, L.ptr(self.q), L.ptr(x), L.ptr(self._scratch), st)
 
     def _relax_repeat(self, lv: Level, rhs, x, nu, x_is_zero):
         """nu x { x += damp * apply(rhs - A x) } (mg.py:268-271), fused
@@ -156,10 +156,12 @@ class MgHierarchy:
         damp = lv.damp
         for it in range(nu):
             if it == 0 and x_is_zero:
-                L.call("vk_patches_apply", h, L.ptr(rhs), L.ptr(x), damp, L.VK_APPLY_XSET, st)
+                L.call("vk_patches_apply", h, L.ptr(rhs), L.ptr(x), damp, L.VK_APPLY_XSET, None,
+                       st)
             else:
                 L.call("vk_residual", lv.A.handle, L.ptr(rhs), L.ptr(x), L.ptr(lv.r), st)
-                L.call("vk_patches_apply", h, L.ptr(lv.r), L.ptr(x), damp, L.VK_APPLY_XADD, st)
+                L.call("vk_patches_apply", h, L.ptr(lv.r), L.ptr(x), damp, L.VK_APPLY_XADD, None,
+                       st)
 
     def _cycle(self, idx, rhs, x, nu, mode):
         if idx == 0:
@@ -256,7 +258,7 @@ def _apply_out(level, r):
     import torch
     out = torch.empty_like(r)
     L.call("vk_patches_apply", level.patches.handle, L.ptr(r), L.ptr(out), 1.0,
-           L.VK_APPLY_OUT, L.stream_ptr())
+           L.VK_APPLY_OUT, None, L.stream_ptr())
     return out
 
 
@@ -280,7 +282,7 @@ def chebyshev_relax(level, b, x, nu, mode: str = "degree"):
     for _ in range(nu):
         L.call("vk_residual", A.handle, L.ptr(bd), L.ptr(xd), L.ptr(r), st)
         L.call("vk_patches_apply", level.patches.handle, L.ptr(r), L.ptr(xd), damp,
-               L.VK_APPLY_XADD, st)
+               L.VK_APPLY_XADD, None, st)
     return to_host(xd, host)
 
 

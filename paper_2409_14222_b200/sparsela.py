@@ -154,21 +154,38 @@ def _destroy_csr(h):
 _CSR_CACHE: dict = {}
 
 
+def _fingerprint(a):
+    """Cheap identity of a host CSR's contents: array addresses, sizes and a
+    strided sample of the values/indices (<= 4,096 of each), so an in-place
+    change such as ``A.data *= 2`` or a reassigned ``A.data`` is seen."""
+    try:
+        data, ind, ptr = a.data, a.indices, a.indptr
+    except AttributeError:
+        return None
+    step = max(1, data.size // 4096)
+    return (a.shape, data.size, data.ctypes.data, ind.ctypes.data, ptr.ctypes.data,
+            hash(data[::step].tobytes()), hash(ind[::step].tobytes()),
+            hash(ptr[::max(1, ptr.size // 4096)].tobytes()))
+
+
 def device_csr(a) -> DeviceCSR:
     """Device copy of a host CSR, cached per host object (the reference
-    passes the same scipy matrix to every call)."""
+    passes the same scipy matrix to every call) and revalidated by a cheap
+    content fingerprint on every lookup: the reference always reads the live
+    scipy matrix, so a matrix changed in place gets a fresh device copy."""
     if isinstance(a, DeviceCSR):
         return a
     key = id(a)
+    fp = _fingerprint(a)
     hit = _CSR_CACHE.get(key)
-    if hit is not None and hit[0]() is a:
+    if hit is not None and hit[0]() is a and hit[2] == fp:
         return hit[1]
     d = DeviceCSR(a)
     try:
         ref = weakref.ref(a, lambda _r, k=key: _CSR_CACHE.pop(k, None))
     except TypeError:
         return d
-    _CSR_CACHE[key] = (ref, d)
+    _CSR_CACHE[key] = (ref, d, fp)
     return d
 
 
@@ -257,13 +274,15 @@ class NullspaceProjector:
         torch = _torch()
         self._qd = [torch.from_numpy(np.ascontiguousarray(q[:, c])).cuda()
                     for c in range(q.shape[1])]
-        self._scratch = torch.zeros(1, dtype=torch.float64, device="cuda")
+        self._scratch = L.reduce_scratch()[0]
 
-    def apply_(self, xd):
-        """In-place projection of a CUDA vector."""
+    def apply_(self, xd, scratch=None):
+        """In-place projection of a CUDA vector.  ``scratch`` (a
+        ``VK_REDUCE_SCRATCH`` device buffer) must be the caller's own when
+        projections may run concurrently on several streams."""
+        sc = self._scratch if scratch is None else scratch
         for qc in self._qd:
-            L.call("vk_project", xd.numel(), L.ptr(qc), L.ptr(xd), L.ptr(self._scratch),
-                   _stream())
+            L.call("vk_project", xd.numel(), L.ptr(qc), L.ptr(xd), L.ptr(sc), _stream())
         return xd
 
     def __call__(self, x):
@@ -322,6 +341,7 @@ class FgmresWorkspace:
         self.zmat = torch.zeros((max_it, n), dtype=torch.float64, device="cuda")
         self.w = torch.empty(n, dtype=torch.float64, device="cuda")
         self.scal = torch.zeros(max_it + 3, dtype=torch.float64, device="cuda")
+        self.red = L.reduce_scratch()[0]      # this workspace's reduction scratch
         self.graphs = {}
         self._key = None
 
@@ -371,6 +391,10 @@ def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
     torch = _torch()
     op = _device_operator(a)
     prec = _device_operator(preconditioner) if preconditioner is not None else None
+    ws = workspace
+    # reduction scratch owned by this solve (or its workspace): solves running
+    # concurrently on different streams never share reduction state
+    red = ws.red if ws is not None else L.reduce_scratch()[0]
     if nullspace is not None and not isinstance(nullspace, NullspaceProjector):
         proj_host = nullspace
 
@@ -379,7 +403,8 @@ def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
             return v
         proj._device = False
     elif nullspace is not None:
-        proj = nullspace.apply_
+        def proj(v, _ns=nullspace):
+            return _ns.apply_(v, red)
     else:
         def proj(v):
             return v
@@ -395,7 +420,7 @@ def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
         proj(r)
     else:
         r = b_.clone()
-    L.call("vk_nrm2", n, L.ptr(r), L.ptr(scal[max_it + 2:]), st)
+    L.call("vk_nrm2", n, L.ptr(r), L.ptr(scal[max_it + 2:]), L.ptr(red), st)
     beta = float(scal[max_it + 2].item())
     base = float(target_norm) if target_norm is not None else beta
     if base == 0.0:
@@ -405,6 +430,8 @@ def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
         return to_host(x, host), KrylovReport(0, history[0], True, np.array(history))
 
     ws = workspace if (workspace is not None and workspace.fits(n, max_it)) else None
+    if ws is None and workspace is not None:
+        red = red.clone()            # a mismatched workspace keeps nothing shared
     if ws is not None:
         vmat, zmat, w = ws.vmat, ws.zmat, ws.w
         ws.scal[max_it + 2:max_it + 3].copy_(scal[max_it + 2:max_it + 3])
@@ -430,18 +457,18 @@ def fgmres(a, b, *, preconditioner=None, rtol: float = 1e-10, max_it: int = 100,
         wz = op(zmat[j])
         w.copy_(wz)
         proj(w)
-        L.call("vk_nrm2", n, L.ptr(w), L.ptr(scal[max_it + 1:]), s_)      # wnorm0
+        L.call("vk_nrm2", n, L.ptr(w), L.ptr(scal[max_it + 1:]), L.ptr(red), s_)  # wnorm0
         # MGS (sparsela.py:160-163): h_0 = v_0.w, then for each i the update
         # w -= h_i v_i fused with the next dot (v_{i+1}.w, or ||w|| after the
         # last one) -- bit-identical to separate dot / axpy / nrm2 kernels
-        L.call("vk_dot", n, L.ptr(vmat[0]), L.ptr(w), L.ptr(scal[0:]), s_)
+        L.call("vk_dot", n, L.ptr(vmat[0]), L.ptr(w), L.ptr(scal[0:]), L.ptr(red), s_)
         for i in range(j + 1):
             if i < j:
                 L.call("vk_axpy_dot", n, L.ptr(scal[i:]), L.ptr(vmat[i]), L.ptr(w),
-                       L.ptr(vmat[i + 1]), L.ptr(scal[i + 1:]), 0, s_)
+                       L.ptr(vmat[i + 1]), L.ptr(scal[i + 1:]), 0, L.ptr(red), s_)
             else:
                 L.call("vk_axpy_dot", n, L.ptr(scal[i:]), L.ptr(vmat[i]), L.ptr(w),
-                       L.ptr(w), L.ptr(scal[j + 1:]), 1, s_)
+                       L.ptr(w), L.ptr(scal[j + 1:]), 1, L.ptr(red), s_)
         L.call("vk_div_dev", n, L.ptr(w), L.ptr(scal[j + 1:]), L.ptr(vmat[j + 1]), s_)
 
     converged = False
@@ -514,15 +541,16 @@ def estimate_lambda_max(a, *, m: int = 10, seed: int = 0, preconditioner=None,
     vmat = torch.zeros((m + 1, n), dtype=torch.float64, device="cuda")
     vmat[0].copy_(torch.from_numpy(v))
     scal = torch.zeros(m + 2, dtype=torch.float64, device="cuda")
+    red = L.reduce_scratch()[0]
     hess = np.zeros((m + 1, m))
     used = 0
     for j in range(m):
         z = prec(vmat[j]) if prec is not None else vmat[j]
         w = op(z).clone()
         for i in range(j + 1):
-            L.call("vk_dot", n, L.ptr(vmat[i]), L.ptr(w), L.ptr(scal[i:]), st)
+            L.call("vk_dot", n, L.ptr(vmat[i]), L.ptr(w), L.ptr(scal[i:]), L.ptr(red), st)
             L.call("vk_axpy_dev", n, L.ptr(scal[i:]), L.ptr(vmat[i]), L.ptr(w), st)
-        L.call("vk_nrm2", n, L.ptr(w), L.ptr(scal[j + 1:]), st)
+        L.call("vk_nrm2", n, L.ptr(w), L.ptr(scal[j + 1:]), L.ptr(red), st)
         hs = scal.cpu().numpy()
         hess[:j + 2, j] = hs[:j + 2]
         used = j + 1

@@ -101,6 +101,16 @@ class PatchSet:
 
     # -- reference attributes -------------------------------------------------
     @property
+    def zbuf_size(self) -> int:
+        """Entries of a caller-owned correction buffer for :func:`apply_additive`."""
+        self.handle
+        return max(int(self._total), 1)
+
+    def new_zbuf(self):
+        import torch
+        return torch.empty(self.zbuf_size, dtype=torch.float64, device="cuda")
+
+    @property
     def num_patches(self) -> int:
         if self._patches is not None:
             return len(self._patches)
@@ -142,9 +152,11 @@ class PatchSet:
         return self._patches
 
     def entity_of(self, p: int):
-        if self._entities is None:
-            return self.patches[p].entity
+        """Entity of kept patch ``p`` (device patch index; size-0 input
+        patches are dropped on the device, ``candidate`` maps back)."""
         cand = self.export()["candidate"]
+        if self._entities is None:
+            return self.patches[int(cand[p])].entity
         return self._entities[cand[p]]
 
 
@@ -335,13 +347,16 @@ def factor_patches(patchset: PatchSet, system) -> PatchSet:
 
 
 def apply_additive(patchset: PatchSet, residual, out=None, *, scale: float = 1.0,
-                   mode: int = L.VK_APPLY_OUT):
+                   mode: int = L.VK_APPLY_OUT, zbuf=None):
     """Weighted sum of exact local solves, sum_i R_i^T W_i A_i^{-1} R_i r
     (reference ``vanka.apply_additive``, ``vanka.py:142-148``).
 
     numpy in -> numpy out (host copies inside); CUDA tensor in -> CUDA tensor
     out.  ``mode``/``scale`` expose the fused damped-update epilogues used by
-    the smoother (``x = scale*out`` / ``x += scale*out``)."""
+    the smoother (``x = scale*out`` / ``x += scale*out``).  ``zbuf`` (a CUDA
+    float64 tensor of :meth:`PatchSet.zbuf_size` entries) holds the per-patch
+    corrections; sweeps of one patch set that may run concurrently on
+    different streams each need their own (default: the set's buffer)."""
     import torch
     if not patchset.factored:
         raise ValueError("patches must be factored before apply_additive")
@@ -350,8 +365,11 @@ def apply_additive(patchset: PatchSet, residual, out=None, *, scale: float = 1.0
         raise ValueError(f"residual has {rd.numel()} entries, patch set needs {patchset.size}")
     if out is None:
         out = torch.empty_like(rd)
+    if zbuf is not None and (zbuf.numel() < patchset.zbuf_size or zbuf.dtype != torch.float64
+                             or not zbuf.is_cuda):
+        raise ValueError(f"zbuf needs {patchset.zbuf_size} CUDA float64 entries")
     L.call("vk_patches_apply", patchset.handle, L.ptr(rd), L.ptr(out), scale, mode,
-           L.stream_ptr())
+           L.ptr(zbuf), L.stream_ptr())
     return to_host(out, host)
 
 
@@ -403,7 +421,7 @@ class SweepStream:
                 if self._used[q]:
                     self.s_comp.wait_event(self.ev_out[q])     # slot's result drained
                 L.call("vk_patches_apply", h, L.ptr(self.r_dev[q]), L.ptr(self.o_dev[q]),
-                       self.scale, self.mode, self.s_comp.cuda_stream)
+                       self.scale, self.mode, None, self.s_comp.cuda_stream)
                 self.ev_comp[q].record(self.s_comp)
             with torch.cuda.stream(self.s_out):
                 self.s_out.wait_event(self.ev_comp[q])

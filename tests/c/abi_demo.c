@@ -77,7 +77,7 @@ int main(void) {
       cudaMalloc((void**)&dres, sizeof out))
     return 2;
   cudaMemcpy(dr, r, sizeof r, cudaMemcpyHostToDevice);
-  CK(vk_patches_apply(P, dr, dout, 1.0, VK_APPLY_OUT, NULL));
+  CK(vk_patches_apply(P, dr, dout, 1.0, VK_APPLY_OUT, NULL, NULL));
   CK(vk_device_sync());
   cudaMemcpy(out, dout, sizeof out, cudaMemcpyDeviceToHost);
 

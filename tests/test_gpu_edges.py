@@ -172,17 +172,20 @@ def test_fused_mgs_step_bit_identical(V, n):
     w0 = torch.from_numpy(rng.standard_normal(n)).cuda()
     a = torch.tensor([0.37], dtype=torch.float64, device="cuda")
     st = L.stream_ptr()
+    red = L.reduce_scratch()[0]
     for sqrt_out in (0, 1):
         w1, w2 = w0.clone(), w0.clone()
         o1 = torch.zeros(1, dtype=torch.float64, device="cuda")
         o2 = torch.zeros(1, dtype=torch.float64, device="cuda")
         L.call("vk_axpy_dev", n, L.ptr(a), L.ptr(x), L.ptr(w1), st)
         if sqrt_out:
-            L.call("vk_nrm2", n, L.ptr(w1), L.ptr(o1), st)
-            L.call("vk_axpy_dot", n, L.ptr(a), L.ptr(x), L.ptr(w2), L.ptr(w2), L.ptr(o2), 1, st)
+            L.call("vk_nrm2", n, L.ptr(w1), L.ptr(o1), L.ptr(red), st)
+            L.call("vk_axpy_dot", n, L.ptr(a), L.ptr(x), L.ptr(w2), L.ptr(w2), L.ptr(o2), 1,
+                   L.ptr(red), st)
         else:
-            L.call("vk_dot", n, L.ptr(x2), L.ptr(w1), L.ptr(o1), st)
-            L.call("vk_axpy_dot", n, L.ptr(a), L.ptr(x), L.ptr(w2), L.ptr(x2), L.ptr(o2), 0, st)
+            L.call("vk_dot", n, L.ptr(x2), L.ptr(w1), L.ptr(o1), L.ptr(red), st)
+            L.call("vk_axpy_dot", n, L.ptr(a), L.ptr(x), L.ptr(w2), L.ptr(x2), L.ptr(o2), 0,
+                   L.ptr(red), st)
         torch.cuda.synchronize()
         assert torch.equal(w1, w2)
         assert o1.cpu().numpy().view(np.uint64)[0] == o2.cpu().numpy().view(np.uint64)[0]
@@ -213,3 +216,76 @@ def test_refactor_reuses_schedule_and_tracks_values(V, name):
     halved = [patch_inverses(ps, p, 1)[0] for p in pick]
     for a, h in zip(first, halved):
         assert np.array_equal((a * 0.5).view(np.uint64), h.view(np.uint64))
+
+
+def _uniform_patch_system(npatch, s, seed):
+    """Diagonally dominant sparse matrix + `npatch` random sorted patches of
+    exactly `s` DoFs (every block is nonsingular)."""
+    rng = np.random.default_rng(seed)
+    n = 4 * npatch + s
+    a = sp.random(n, n, density=8.0 / n, random_state=seed, format="csr")
+    a = (a + a.T + sp.diags(np.full(n, 40.0))).tocsr()
+    a.sort_indices()
+    idx = [np.sort(rng.choice(n, size=s, replace=False)) for _ in range(npatch)]
+    return a, idx
+
+
+def _dense_sweep(a, idx, r, weights):
+    out = np.zeros(a.shape[0])
+    ad = a.toarray()
+    for ii, w in zip(idx, weights):
+        if ii.size == 0:
+            continue
+        out[ii] += w * np.linalg.solve(ad[np.ix_(ii, ii)], r[ii])
+    return out
+
+
+@pytest.mark.parametrize("s", [16, 29])
+def test_bulk_kernel_uniform_small_patches(V, s):
+    """>= 4,736 uniform patches of s <= 30 take the TMA bulk-copy sweep with
+    one row slot per lane (R = 1); lanes past s must not read past their
+    shared-memory stage: the result matches a dense solve."""
+    npatch = 5000
+    a, idx = _uniform_patch_system(npatch, s, seed=s)
+    ps = V.PatchSet([V.Patch(None, ii, s, np.ones(s)) for ii in idx], a.shape[0],
+                    None, "unit")
+    V.factor_patches(ps, a)
+    r = np.random.default_rng(1).uniform(-1, 1, a.shape[0])
+    got = V.apply_additive(ps, r)
+    ref = _dense_sweep(a, idx, r, [np.ones(s)] * npatch)
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_zero_size_patches_are_dropped(V):
+    """Hand-built patch lists may hold size-0 patches (the reference's
+    apply_additive skips them, lu_solve of s=0 is empty); the device handle
+    drops them and keeps the input position for entity lookup."""
+    a, idx = _uniform_patch_system(40, 7, seed=3)
+    pats, ents = [], []
+    for k, ii in enumerate(idx):
+        if k % 5 == 0:
+            pats.append(V.Patch(("empty", k), np.zeros(0, np.int64), 0, np.ones(0)))
+        pats.append(V.Patch(("p", k), ii, 7, np.ones(7)))
+    ps = V.PatchSet(pats, a.shape[0], None, "unit")
+    V.factor_patches(ps, a)
+    ex = ps.export()
+    assert len(ex["offsets"]) - 1 == 40
+    assert all(ps.entity_of(p)[0] == "p" for p in range(40))
+    assert [ps.entity_of(p)[1] for p in range(40)] == list(range(40))
+    r = np.random.default_rng(2).uniform(-1, 1, a.shape[0])
+    got = V.apply_additive(ps, r)
+    ref = _dense_sweep(a, idx, r, [np.ones(7)] * 40)
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_device_csr_cache_follows_in_place_changes(V):
+    """The reference reads the live scipy matrix on every call; the device
+    copy cache must notice ``A.data *= 2``."""
+    a = sp.random(500, 500, density=0.02, random_state=4, format="csr") + sp.eye(500)
+    a = a.tocsr()
+    x = np.random.default_rng(0).standard_normal(500)
+    y1 = V.spmv(a, x)
+    a.data *= 2.0
+    y2 = V.spmv(a, x)
+    assert np.array_equal(y2, 2.0 * y1)
+    assert np.array_equal(y2, a @ x)

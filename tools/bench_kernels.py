@@ -78,8 +78,8 @@ def main():
         x = torch.zeros_like(r)
         y = torch.zeros_like(r)
         h = ps.handle
-        t_solve = timed(lambda: L.call("vk_patches_solve", h, L.ptr(r), sp_), args.reps, st)
-        t_acc = timed(lambda: L.call("vk_patches_accumulate", h, L.ptr(x), 0.5, L.VK_APPLY_XADD, sp_),
+        t_solve = timed(lambda: L.call("vk_patches_solve", h, L.ptr(r), None, sp_), args.reps, st)
+        t_acc = timed(lambda: L.call("vk_patches_accumulate", h, None, L.ptr(x), 0.5, L.VK_APPLY_XADD, sp_),
                       args.reps, st)
         t_res = timed(lambda: L.call("vk_residual", A.handle, L.ptr(r), L.ptr(x), L.ptr(y), sp_),
                       args.reps, st)
