@@ -140,6 +140,9 @@ VK_API int vk_patches_apply(vk_patches_t h, const double* r, double* out, double
 VK_API int vk_patches_solve(vk_patches_t h, const double* r, double* zbuf, void* stream);
 VK_API int vk_patches_accumulate(vk_patches_t h, const double* zbuf, double* out, double scale,
                                  int32_t mode, void* stream);
+/* name of the K4a kernel vk_patches_solve launches for this patch set (for
+ * profiling tools and the bench line) */
+VK_API const char* vk_patches_solve_kernel(vk_patches_t h);
 VK_API int vk_patches_destroy(vk_patches_t h);
 
 /* ---------------- dense / vector helpers (FGMRES + V-cycle plumbing) -------
@@ -182,6 +185,31 @@ VK_API int vk_combine(int64_t n, int32_t count, const double* z, const double* c
                double* x, void* stream);
 /* dense[rows x cols] (row-major, device) = CSR (coarse operator densify) */
 VK_API int vk_csr_to_dense(vk_csr_t a, double* dense, void* stream);
+
+/* ---------------- coarse dense operator and its inverse --------------------
+ * replaces the reference's coarse factorization (mg.py:228-232:
+ * lu_factor(A0.toarray() + shift * np.outer(q, q))), applied per V-cycle as
+ * x = M^{-1} b by vk_gemv (mg.py:274-279 applies getrs).
+ * vk_coarse_operator: dense row-major M = A0 + shift q q^T, formed exactly as
+ * numpy does (fl(a + fl(shift * fl(q_i q_j))), bit-identical).
+ * vk_dense_inverse: explicit inverse of a DEVICE row-major n x n matrix by
+ * blocked Gauss-Jordan elimination with partial pivoting (LAPACK pivot
+ * order); `work` is a DEVICE buffer of vk_dense_inverse_workspace(n) bytes.
+ * The reference guard of sparsela.lu_factor (sparsela.py:76-83) applies:
+ * returns VK_SINGULAR with *reason = VK_PATCH_ZERO_ROW (all-zero row
+ * *singular_at) or VK_PATCH_SMALL_PIVOT (|pivot of column *singular_at| <
+ * 1e-12 x its source row's magnitude).  Synchronises `stream`. */
+VK_API int vk_coarse_operator(vk_csr_t a, const double* q, double shift, double* dense,
+                              void* stream);
+VK_API int64_t vk_dense_inverse_workspace(int32_t n);
+/* the factorization alone (sparsela.lu_factor, sparsela.py:63-84, for a dense
+ * DEVICE matrix): lu = packed L\U (row-major, unit L below the diagonal),
+ * ipiv_host[n] (may be NULL) = LAPACK's 0-based swap sequence; same guard,
+ * workspace and synchronisation as vk_dense_inverse. */
+VK_API int vk_dense_lu(int32_t n, const double* a, double* lu, int32_t* ipiv_host, void* work,
+                       int32_t* reason, int32_t* singular_at, void* stream);
+VK_API int vk_dense_inverse(int32_t n, const double* a, double* inv, void* work,
+                            int32_t* reason, int32_t* singular_at, void* stream);
 
 #ifdef __cplusplus
 }

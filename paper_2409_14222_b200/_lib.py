@@ -50,6 +50,7 @@ SIGNATURES = {
     "vk_patches_apply": (C.c_int, [_p, _p, _p, _f64, _i32, _p, _p]),
     "vk_patches_solve": (C.c_int, [_p, _p, _p, _p]),
     "vk_patches_accumulate": (C.c_int, [_p, _p, _p, _f64, _i32, _p]),
+    "vk_patches_solve_kernel": (C.c_char_p, [_p]),
     "vk_patches_destroy": (C.c_int, [_p]),
     "vk_dot": (C.c_int, [_i64, _p, _p, _p, _p, _p]),
     "vk_axpy_dev": (C.c_int, [_i64, _p, _p, _p, _p]),
@@ -62,6 +63,10 @@ SIGNATURES = {
     "vk_gemv": (C.c_int, [_i32, _i32, _p, _p, _p, _p]),
     "vk_combine": (C.c_int, [_i64, _i32, _p, _p, _p, _p]),
     "vk_csr_to_dense": (C.c_int, [_p, _p, _p]),
+    "vk_coarse_operator": (C.c_int, [_p, _p, _f64, _p, _p]),
+    "vk_dense_inverse_workspace": (C.c_int64, [_i32]),
+    "vk_dense_inverse": (C.c_int, [_i32, _p, _p, _p, _P_i32, _P_i32, _p]),
+    "vk_dense_lu": (C.c_int, [_i32, _p, _p, _p, _p, _P_i32, _P_i32, _p]),
 }
 
 _lib = None

@@ -17,7 +17,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libvanka_b200.so")
-SOURCES = ["vk_csr.cu", "vk_patches.cu", "vk_factor.cu", "vk_apply.cu", "vk_blas.cu"]
+SOURCES = ["vk_csr.cu", "vk_patches.cu", "vk_factor.cu", "vk_apply.cu", "vk_blas.cu",
+           "vk_dense.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -637,6 +637,22 @@ static bool chunk_enabled() {
   return v;
 }
 
+// which K4a kernel a patch set runs (same decisions as vk_patches_solve)
+static const char* solve_kernel_name(const vk_patches_s* h) {
+  const int rpl = (h->smax + 31) / 32;
+  if (h->npatch == 0) return "none";
+  if (h->npatch < 148 * kApplyWarps * 4 && rpl <= 4) return "patch_solve_split_kernel";
+  if (h->smax <= kBulkMaxS && !h->mixed_sizes && bulk_enabled() &&
+      bulk_smem(h->smax) <= size_t(kBulkDynMax))
+    return "patch_solve_bulk_kernel";
+  if (h->smax <= 128 && chunk_enabled()) return "patch_solve_chunk_kernel";
+  return "patch_solve_kernel";
+}
+
+extern "C" const char* vk_patches_solve_kernel(vk_patches_t h) {
+  return h ? solve_kernel_name(h) : "none";
+}
+
 extern "C" int vk_patches_solve(vk_patches_t h, const double* r, double* zbuf, void* stream) {
   if (int st = check_apply(h)) return st;
   VK_REQUIRE(r, "vk_patches_solve: null residual");

@@ -1,0 +1,669 @@
+// Dense coarse-level operator and its explicit inverse, hand-written
+// (replaces the reference's coarse factorization: mg.py:228-232 builds
+// A0 + max|A0| q q^T and factors it with sparsela.lu_factor = LAPACK getrf +
+// the pivot guard; mg.py:274-279 applies it with getrs between two
+// projections).
+//
+// The inverse is applied once per V-cycle as a bandwidth-bound GEMV
+// (vk_gemv), so the setup forms M^{-1} explicitly, the LAPACK way
+// (getrf, then the getrs solve L U X = I, then the column permutation):
+//
+//   A. blocked right-looking LU with partial pivoting, panel width 32:
+//      1. the panel W[k0:, K] (K = [k0, k0 + 32)) is copied to P;
+//      2. one cooperative kernel factors it (getf2 order: pivot = first
+//         maximum |a| among the open positions — LAPACK idamax — row
+//         interchange, multipliers scaled by the pivot reciprocal, rank-1
+//         update of the panel's trailing columns; one grid barrier per column,
+//         the next column's pivot candidates found while the rows are
+//         updated) and checks the reference guard |u_kk| >= 1e-12 * the
+//         magnitude of the pivot's source row (sparsela.py:76-83);
+//      3. the interchanges are applied to the rest of the rows (laswp) and
+//         the factored panel written back;
+//      4. U12 = L11^{-1} A12 (unit lower substitution, one thread per column);
+//      5. A22 -= L21 U12 — DFMA register-tiled GEMM.
+//   B. X = U^{-1} L^{-1}: forward substitution L Y = I blockwise (Y lower
+//      triangular: only the columns left of the block are touched), then
+//      backward substitution U X = Y (substitution of the 32-row block, GEMM
+//      update of the rows above);
+//   C. inverse = X P (column permutation undone while gathering the output).
+//
+// 2 n^3 flops in total; everything deterministic (fixed tiles and summation
+// orders).  The coarse matrix itself is formed exactly like numpy's
+// a0.toarray() + shift * np.outer(q, q) (bit-identical, mg.py:229-232).
+#include <algorithm>
+#include <cooperative_groups.h>
+
+#include "vk_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int kNB = 32;          // panel / block width (= lanes: one column per lane)
+constexpr int kPanelThreads = 256;
+
+// M[i, j] = fl(A0[i, j] + fl(shift * fl(q_i * q_j)))   (absent A0 entries: +0.0)
+__global__ void __launch_bounds__(256) coarse_operator_kernel(
+    int n, const int* __restrict__ ptr, const int* __restrict__ ind,
+    const double* __restrict__ val, const double* __restrict__ q, double shift,
+    double* __restrict__ m) {
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const double qi = q[i];
+    double* row = m + int64_t(i) * n;
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+      row[j] = __dadd_rn(0.0, __dmul_rn(shift, __dmul_rn(qi, q[j])));
+    __syncthreads();
+    for (int k = ptr[i] + threadIdx.x; k < ptr[i + 1]; k += blockDim.x) {
+      const int j = ind[k];
+      row[j] = __dadd_rn(val[k], __dmul_rn(shift, __dmul_rn(qi, q[j])));
+    }
+    __syncthreads();
+  }
+}
+
+// rowscale[i] = max_j |M[i, j]|, rowid[i] = i; an all-zero row is reported
+// like the reference (sparsela.py:76-78)
+__global__ void __launch_bounds__(256) row_scale_kernel(int n, const double* __restrict__ m,
+                                                        double* __restrict__ scale,
+                                                        int* __restrict__ rowid,
+                                                        int* __restrict__ status) {
+  __shared__ double sh[8];
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    double v = 0.0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) v = fmax(v, fabs(m[int64_t(i) * n + j]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < 8; ++w) v = fmax(v, sh[w]);
+      scale[i] = v;
+      rowid[i] = i;
+      if (v == 0.0 && atomicCAS(status, 0, VK_PATCH_ZERO_ROW) == 0) status[1] = i;
+    }
+    __syncthreads();
+  }
+}
+
+// P[i, s] = W[k0 + i, k0 + s] for the m = n - k0 open rows (s < nbk), 0 beyond
+__global__ void panel_copy_kernel(int n, int k0, int nbk, const double* __restrict__ w,
+                                  double* __restrict__ p) {
+  const int m = n - k0;
+  const int64_t total = int64_t(m) * kNB;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / kNB), s = static_cast<int>(e % kNB);
+    p[e] = (s < nbk) ? w[int64_t(k0 + i) * n + k0 + s] : 0.0;
+  }
+}
+
+struct PanelBufs {
+  double* candv;    // [2][G]   |value| of each CTA's best position (-1: none)
+  int* candi;       // [2][G]   that position (panel coordinates)
+  double* candrow;  // [2][G][kNB] the best position's panel row
+  double* krow;     // [2][kNB] the row at the current pivot position
+  int* candid;      // [2][G]   original row of each CTA's candidate
+  int* krowid;      // [2]      original row at the current pivot position
+  int* ipiv;        // [n]      swap sequence (global positions)
+  int* rowid;       // [n]      original row at each global position
+  const double* rowscale;  // [n] max |M[r, :]| of original row r
+  int* status;      // [2]: reason (0 ok, VK_PATCH_ZERO_ROW / VK_PATCH_SMALL_PIVOT), column
+};
+
+// lexicographic argmax: larger |v|; on ties the lower position (LAPACK idamax)
+__device__ __forceinline__ bool better(double v, int i, double bv, int bi) {
+  return v > bv || (v == bv && i < bi);
+}
+
+__device__ __forceinline__ void warp_argmax(double& v, int& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+    if (better(ov, oi, v, i)) {
+      v = ov;
+      i = oi;
+    }
+  }
+}
+
+// CTA-wide argmax of (v, i); result in (*bv, *bi) for all threads
+__device__ void block_argmax(double v, int i, double* shv, int* shi, double* bv, int* bi) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  warp_argmax(v, i);
+  __syncthreads();
+  if (lane == 0) {
+    shv[warp] = v;
+    shi[warp] = i;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int nw = kPanelThreads / 32;
+    v = lane < nw ? shv[lane] : -1.0;
+    i = lane < nw ? shi[lane] : 0x7fffffff;
+    warp_argmax(v, i);
+    if (lane == 0) {
+      shv[nw] = v;
+      shi[nw] = i;
+    }
+  }
+  __syncthreads();
+  *bv = shv[kPanelThreads / 32];
+  *bi = shi[kPanelThreads / 32];
+}
+
+// LU with partial pivoting of the m x kNB panel P (row-major, panel
+// coordinates; global position = k0 + i), nbk <= kNB steps.  CTA c owns the
+// positions [c*rows, (c+1)*rows); warp w of a CTA the positions lo + w,
+// lo + w + 8, ...; lane s holds column s.
+__global__ void __launch_bounds__(kPanelThreads) panel_lu_kernel(int m, int k0, int nbk,
+                                                                 double* __restrict__ P,
+                                                                 PanelBufs b) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double shv[kPanelThreads / 32 + 1];
+  __shared__ int shi[kPanelThreads / 32 + 1];
+  __shared__ double prow[kNB], krw[kNB];
+  __shared__ int sh_p, sh_pc, sh_bad;
+  const int G = gridDim.x;
+  const int c = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int nw = kPanelThreads / 32;
+  const int rows = (m + G - 1) / G;
+  const int lo = min(m, c * rows), hi = min(m, lo + rows);
+  if (__ldcg(b.status)) return;  // singular earlier (uniform across CTAs)
+
+  // publish this CTA's best candidate for column kk (positions >= kk)
+  auto publish = [&](int kk, int par) {
+    double v = -1.0;
+    int bi = 0x7fffffff;
+    for (int i = max(lo, kk) + warp; i < hi; i += nw) {
+      const double a = fabs(P[int64_t(i) * kNB + kk]);
+      if (better(a, i, v, bi)) {
+        v = a;
+        bi = i;
+      }
+    }
+    double bv;
+    int bpos;
+    block_argmax(v, bi, shv, shi, &bv, &bpos);
+    if (threadIdx.x == 0) {
+      b.candv[par * G + c] = bv;
+      b.candi[par * G + c] = bpos;
+      if (bv >= 0.0) b.candid[par * G + c] = b.rowid[k0 + bpos];
+      if (kk >= lo && kk < hi) b.krowid[par] = b.rowid[k0 + kk];
+    }
+    if (bv >= 0.0 && threadIdx.x < kNB)
+      b.candrow[(int64_t(par) * G + c) * kNB + threadIdx.x] = P[int64_t(bpos) * kNB + threadIdx.x];
+    if (kk >= lo && kk < hi && threadIdx.x < kNB)
+      b.krow[par * kNB + threadIdx.x] = P[int64_t(kk) * kNB + threadIdx.x];
+  };
+
+  publish(0, 0);
+  grid.sync();
+  for (int kk = 0; kk < nbk; ++kk) {
+    const int par = kk & 1;
+    {
+      // global pivot: every CTA reduces the G published candidates
+      double v = -1.0;
+      int bi = 0x7fffffff, bc = 0;
+      for (int cc = threadIdx.x; cc < G; cc += kPanelThreads) {
+        const double cv = __ldcg(b.candv + par * G + cc);   // other CTAs' data: L2
+        const int ci = __ldcg(b.candi + par * G + cc);
+        if (cv >= 0.0 && better(cv, ci, v, bi)) {
+          v = cv;
+          bi = ci;
+          bc = cc;
+        }
+      }
+      double bv;
+      int bpos;
+      block_argmax(v, bi, shv, shi, &bv, &bpos);
+      if (bi == bpos && v == bv && v >= 0.0) sh_pc = bc;   // the owner of that position
+      if (threadIdx.x == 0) sh_p = bpos;
+      __syncthreads();
+      // the reference guard (sparsela.py:79-83)
+      if (threadIdx.x == 0) {
+        const int orig = __ldcg(b.candid + par * G + sh_pc);
+        sh_bad = !(bv >= 1e-12 * b.rowscale[orig]) || !isfinite(bv);
+      }
+      __syncthreads();
+    }
+    const int p = sh_p;
+    if (sh_bad) {
+      if (c == 0 && threadIdx.x == 0) {
+        b.status[0] = VK_PATCH_SMALL_PIVOT;
+        b.status[1] = k0 + kk;
+      }
+      return;   // uniform: every CTA saw the same candidates
+    }
+    const int pc = sh_pc;
+    const int p_id = __ldcg(b.candid + par * G + pc), k_id = __ldcg(b.krowid + par);
+    if (threadIdx.x < kNB) {
+      krw[threadIdx.x] = __ldcg(b.krow + par * kNB + threadIdx.x);
+      prow[threadIdx.x] = __ldcg(b.candrow + (int64_t(par) * G + pc) * kNB + threadIdx.x);
+    }
+    if (c == 0 && threadIdx.x == 0) b.ipiv[k0 + kk] = k0 + p;
+    if (threadIdx.x == 0) {   // interchange the original-row labels (owners)
+      if (kk >= lo && kk < hi) b.rowid[k0 + kk] = p_id;
+      if (p != kk && p >= lo && p < hi) b.rowid[k0 + p] = k_id;
+    }
+    __syncthreads();
+    const double rcp = 1.0 / prow[kk];
+    // getf2: position kk takes the pivot row; every position below gets
+    // l = a_ik / u_kk (as a * (1/u_kk), dscal) and a_ij -= l u_kj (dger)
+    for (int i = max(lo, kk) + warp; i < hi; i += nw) {
+      double nv;
+      if (i == kk) {
+        nv = prow[lane];
+      } else {
+        const double src = (i == p) ? krw[lane] : P[int64_t(i) * kNB + lane];
+        const double l = __dmul_rn(__shfl_sync(0xffffffffu, src, kk), rcp);
+        nv = (lane < kk) ? src : (lane == kk) ? l : fma(-l, prow[lane], src);
+      }
+      P[int64_t(i) * kNB + lane] = nv;
+    }
+    __syncthreads();
+    if (kk + 1 < nbk) publish(kk + 1, par ^ 1);
+    grid.sync();
+  }
+}
+
+// laswp on the columns outside the panel + write the factored panel back
+__global__ void swap_writeback_kernel(int n, int k0, int nbk, const int* __restrict__ ipiv,
+                                      const int* __restrict__ status, const double* __restrict__ P,
+                                      double* __restrict__ w) {
+  if (__ldcg(status)) return;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    if (j >= k0 && j < k0 + nbk) continue;
+    for (int s = 0; s < nbk; ++s) {
+      const int k = k0 + s, p = ipiv[k];
+      if (p != k) {
+        const double a = w[int64_t(k) * n + j];
+        w[int64_t(k) * n + j] = w[int64_t(p) * n + j];
+        w[int64_t(p) * n + j] = a;
+      }
+    }
+  }
+  const int m = n - k0;
+  const int64_t total = int64_t(m) * nbk;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(e / nbk), s = static_cast<int>(e % nbk);
+    w[int64_t(k0 + i) * n + k0 + s] = P[int64_t(i) * kNB + s];
+  }
+}
+
+// B[0:nbk, j] = L^{-1} B (unit lower nbk x nbk L at l, leading dim ldl), columns
+// j in [0, ncols): x_s = b_s - sum_{r < s} l_sr x_r
+__global__ void __launch_bounds__(128) trsm_lower_unit_kernel(int nbk, const double* __restrict__ l,
+                                                              int64_t ldl, double* __restrict__ bm,
+                                                              int64_t ldb, int ncols,
+                                                              const int* __restrict__ status) {
+  __shared__ double Ls[kNB][kNB + 1];
+  if (__ldcg(status)) return;
+  for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
+    const int r = e / kNB, t = e % kNB;
+    Ls[r][t] = (r < nbk && t < nbk) ? l[r * ldl + t] : 0.0;
+  }
+  __syncthreads();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  double x[kNB];
+#pragma unroll
+  for (int s = 0; s < kNB; ++s) x[s] = (s < nbk) ? bm[s * ldb + j] : 0.0;
+  // dot first, one subtraction (the BLAS kernels' order: the sum of the
+  // products is formed in a register, then taken from the right-hand side)
+#pragma unroll
+  for (int s = 1; s < kNB; ++s) {
+    double t = 0.0;
+#pragma unroll
+    for (int r = 0; r < s; ++r) t = fma(Ls[s][r], x[r], t);
+    x[s] = __dsub_rn(x[s], t);
+  }
+#pragma unroll
+  for (int s = 0; s < kNB; ++s)
+    if (s < nbk) bm[s * ldb + j] = x[s];
+}
+
+// B[0:nbk, j] = U^{-1} B (non-unit upper), rows from the last up:
+// x_k = (b_k - sum_{r > k} u_kr x_r) / u_kk
+__global__ void __launch_bounds__(128) trsm_upper_kernel(int nbk, const double* __restrict__ u,
+                                                         int64_t ldu, double* __restrict__ bm,
+                                                         int64_t ldb, int ncols,
+                                                         const int* __restrict__ status) {
+  __shared__ double Us[kNB][kNB + 1];
+  if (__ldcg(status)) return;
+  for (int e = threadIdx.x; e < kNB * kNB; e += blockDim.x) {
+    const int r = e / kNB, t = e % kNB;
+    Us[r][t] = (r < nbk && t < nbk) ? u[r * ldu + t] : (r == t ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= ncols) return;
+  double x[kNB];
+#pragma unroll
+  for (int s = 0; s < kNB; ++s) x[s] = (s < nbk) ? bm[s * ldb + j] : 0.0;
+#pragma unroll
+  for (int k = kNB - 1; k >= 0; --k) {
+    double t = 0.0;
+#pragma unroll
+    for (int r = k + 1; r < kNB; ++r) t = fma(Us[k][r], x[r], t);
+    x[k] = __ddiv_rn(__dsub_rn(x[k], t), Us[k][k]);
+  }
+#pragma unroll
+  for (int s = 0; s < kNB; ++s)
+    if (s < nbk) bm[s * ldb + j] = x[s];
+}
+
+// C[i, j] -= sum_{s < nbk} A[i, s] B[s, j]   for i < mrows, j < ncols
+// (A: mrows x nbk, lda; B: nbk x ncols, ldb; C: ldc; all row-major).
+// 64 x 64 tile per CTA, 256 threads as 16 x 16, 4 x 4 outputs per thread.
+constexpr int kBM = 64, kBN = 64;
+__global__ void __launch_bounds__(256) gemm_sub_kernel(int mrows, int ncols, int nbk,
+                                                       const double* __restrict__ A, int64_t lda,
+                                                       const double* __restrict__ B, int64_t ldb,
+                                                       double* __restrict__ Cm, int64_t ldc,
+                                                       const int* __restrict__ status) {
+  constexpr int TM = kBM / 16, TN = kBN / 16;
+  __shared__ double As[kNB][kBM + 1];   // transposed: As[s][row]
+  __shared__ double Bs[kNB][kBN];
+  if (__ldcg(status)) return;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int i0 = blockIdx.y * kBM, j0 = blockIdx.x * kBN;
+  for (int e = threadIdx.x; e < kBM * kNB; e += 256) {
+    const int rr = e / kNB, s = e % kNB;
+    const int i = i0 + rr;
+    As[s][rr] = (i < mrows && s < nbk) ? A[i * lda + s] : 0.0;
+  }
+  for (int e = threadIdx.x; e < kNB * kBN; e += 256) {
+    const int s = e / kBN, cc = e % kBN;
+    const int j = j0 + cc;
+    Bs[s][cc] = (j < ncols && s < nbk) ? B[s * ldb + j] : 0.0;
+  }
+  // the products are summed in registers from zero, then subtracted from C
+  // once (BLAS dgemm: C = beta C + alpha (A B)); accumulating onto C instead
+  // rounds every step at |C|'s magnitude and made the coarse inverse of the
+  // ill-conditioned BDM operator 4x less accurate
+  double cin[TM][TN], acc[TM][TN];
+#pragma unroll
+  for (int a = 0; a < TM; ++a) {
+    const int i = i0 + ty + 16 * a;
+#pragma unroll
+    for (int q = 0; q < TN; ++q) {
+      const int j = j0 + tx + 16 * q;
+      cin[a][q] = (i < mrows && j < ncols) ? Cm[i * ldc + j] : 0.0;
+      acc[a][q] = 0.0;
+    }
+  }
+  __syncthreads();
+  for (int s = 0; s < nbk; ++s) {
+    double av[TM], bv[TN];
+#pragma unroll
+    for (int a = 0; a < TM; ++a) av[a] = As[s][ty + 16 * a];
+#pragma unroll
+    for (int q = 0; q < TN; ++q) bv[q] = Bs[s][tx + 16 * q];
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int q = 0; q < TN; ++q) acc[a][q] = fma(av[a], bv[q], acc[a][q]);
+  }
+#pragma unroll
+  for (int a = 0; a < TM; ++a) {
+    const int i = i0 + ty + 16 * a;
+    if (i >= mrows) continue;
+#pragma unroll
+    for (int q = 0; q < TN; ++q) {
+      const int j = j0 + tx + 16 * q;
+      if (j < ncols) Cm[i * ldc + j] = __dsub_rn(cin[a][q], acc[a][q]);
+    }
+  }
+}
+
+__global__ void identity_kernel(int n, double* __restrict__ x) {
+  const int64_t total = int64_t(n) * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x)
+    x[e] = (e / n == e % n) ? 1.0 : 0.0;
+}
+
+// inverse = X P_{n-1} ... P_0: column map from the swap sequence, applied in
+// reverse order by one thread on a shared-memory copy of the map
+__global__ void colmap_kernel(int n, const int* __restrict__ ipiv, const int* __restrict__ status,
+                              int* __restrict__ map) {
+  extern __shared__ int sm[];
+  if (__ldcg(status)) return;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) sm[j] = j;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = n - 1; k >= 0; --k) {
+      const int p = ipiv[k];
+      if (p != k) {
+        const int t = sm[k];
+        sm[k] = sm[p];
+        sm[p] = t;
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) map[j] = sm[j];
+}
+
+__global__ void gather_cols_kernel(int n, const int* __restrict__ map,
+                                   const int* __restrict__ status, const double* __restrict__ x,
+                                   double* __restrict__ out) {
+  if (__ldcg(status)) return;
+  const int64_t total = int64_t(n) * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / n;
+    const int j = static_cast<int>(e - i * n);
+    out[e] = x[i * n + map[j]];
+  }
+}
+
+int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+
+struct Layout {
+  int64_t w, x, p, candv, candi, candrow, krow, candid, krowid, ipiv, rowid, scale, status, map,
+      total;
+};
+
+Layout layout(int n, int G) {
+  Layout L{};
+  int64_t o = 0;
+  L.w = o; o = align256(o + 8 * int64_t(n) * n);
+  L.x = o; o = align256(o + 8 * int64_t(n) * n);
+  L.p = o; o = align256(o + 8 * int64_t(n) * kNB);
+  L.candv = o; o = align256(o + 8 * 2 * int64_t(G));
+  L.candi = o; o = align256(o + 4 * 2 * int64_t(G));
+  L.candrow = o; o = align256(o + 8 * 2 * int64_t(G) * kNB);
+  L.krow = o; o = align256(o + 8 * 2 * kNB);
+  L.candid = o; o = align256(o + 4 * 2 * int64_t(G));
+  L.krowid = o; o = align256(o + 4 * 2);
+  L.ipiv = o; o = align256(o + 4 * int64_t(n));
+  L.rowid = o; o = align256(o + 4 * int64_t(n));
+  L.scale = o; o = align256(o + 8 * int64_t(n));
+  L.status = o; o = align256(o + 8);
+  L.map = o; o = align256(o + 4 * int64_t(n));
+  L.total = o;
+  return L;
+}
+
+// one CTA per SM for the cooperative panel kernel
+int panel_grid() {
+  static std::mutex mu;
+  static std::map<int, int> by_dev;
+  std::lock_guard<std::mutex> lock(mu);
+  const int dev = vk_current_device();
+  auto it = by_dev.find(dev);
+  if (it != by_dev.end()) return it->second;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  by_dev[dev] = sms;
+  return sms;
+}
+
+cudaError_t gemm_sub(int mrows, int ncols, int nbk, const double* A, int64_t lda, const double* B,
+                     int64_t ldb, double* Cm, int64_t ldc, const int* status, cudaStream_t st) {
+  if (mrows <= 0 || ncols <= 0) return cudaSuccess;
+  const dim3 grid((ncols + kBN - 1) / kBN, (mrows + kBM - 1) / kBM);
+  gemm_sub_kernel<<<grid, 256, 0, st>>>(mrows, ncols, nbk, A, lda, B, ldb, Cm, ldc, status);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" int vk_coarse_operator(vk_csr_t a, const double* q, double shift, double* dense,
+                                  void* stream) {
+  VK_REQUIRE(a && q && dense, "vk_coarse_operator: null argument");
+  VK_REQUIRE(a->nrows == a->ncols, "vk_coarse_operator: matrix must be square");
+  if (a->nrows == 0) return VK_OK;
+  coarse_operator_kernel<<<std::min(a->nrows, 148 * 8), 256, 0, vk_stream(stream)>>>(
+      a->nrows, a->indptr, a->indices, a->data, q, shift, dense);
+  VK_CHECK_LAUNCH();
+  return VK_OK;
+}
+
+extern "C" int64_t vk_dense_inverse_workspace(int32_t n) {
+  if (n <= 0) return 0;
+  return layout(n, panel_grid()).total;
+}
+
+namespace {
+
+struct DenseWork {
+  double *W, *X, *P, *scale;
+  int* map;
+  PanelBufs pb;
+};
+
+DenseWork carve(int n, void* work) {
+  const int G = panel_grid();
+  const Layout Lw = layout(n, G);
+  char* base = static_cast<char*>(work);
+  DenseWork d;
+  d.W = reinterpret_cast<double*>(base + Lw.w);
+  d.X = reinterpret_cast<double*>(base + Lw.x);
+  d.P = reinterpret_cast<double*>(base + Lw.p);
+  d.pb.candv = reinterpret_cast<double*>(base + Lw.candv);
+  d.pb.candi = reinterpret_cast<int*>(base + Lw.candi);
+  d.pb.candrow = reinterpret_cast<double*>(base + Lw.candrow);
+  d.pb.krow = reinterpret_cast<double*>(base + Lw.krow);
+  d.pb.candid = reinterpret_cast<int*>(base + Lw.candid);
+  d.pb.krowid = reinterpret_cast<int*>(base + Lw.krowid);
+  d.pb.ipiv = reinterpret_cast<int*>(base + Lw.ipiv);
+  d.pb.rowid = reinterpret_cast<int*>(base + Lw.rowid);
+  d.scale = reinterpret_cast<double*>(base + Lw.scale);
+  d.pb.rowscale = d.scale;
+  d.pb.status = reinterpret_cast<int*>(base + Lw.status);
+  d.map = reinterpret_cast<int*>(base + Lw.map);
+  return d;
+}
+
+// A. blocked LU of a (copied into d.W), asynchronous on st
+int run_lu(int n, const double* a, DenseWork& d, cudaStream_t st) {
+  const int G = panel_grid();
+  const int64_t ld = n;
+  double* W = d.W;
+  double* P = d.P;
+  PanelBufs pb = d.pb;
+  const int* status = pb.status;
+  VK_CHECK_CUDA(cudaMemcpyAsync(W, a, 8 * int64_t(n) * n, cudaMemcpyDeviceToDevice, st));
+  VK_CHECK_CUDA(cudaMemsetAsync(pb.status, 0, 8, st));
+  row_scale_kernel<<<std::min(n, 148 * 8), 256, 0, st>>>(n, W, d.scale, pb.rowid, pb.status);
+  const int vgrid = vk_grid(int64_t(n) * kNB, 256, 148 * 8);
+  const int rgrid = std::max(1, std::min((n + 255) / 256, 148 * 4));
+  for (int k0 = 0; k0 < n; k0 += kNB) {
+    int nbk = std::min(kNB, n - k0);
+    int m = n - k0;
+    panel_copy_kernel<<<vgrid, 256, 0, st>>>(n, k0, nbk, W, P);
+    void* args[] = {&m, &k0, &nbk, &P, &pb};
+    VK_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)panel_lu_kernel, dim3(G),
+                                              dim3(kPanelThreads), args, 0, st));
+    swap_writeback_kernel<<<rgrid, 256, 0, st>>>(n, k0, nbk, pb.ipiv, status, P, W);
+    const int rest = n - k0 - nbk;
+    if (rest > 0) {
+      double* a12 = W + int64_t(k0) * ld + k0 + nbk;
+      trsm_lower_unit_kernel<<<(rest + 127) / 128, 128, 0, st>>>(
+          nbk, W + int64_t(k0) * ld + k0, ld, a12, ld, rest, status);
+      VK_CHECK_CUDA(gemm_sub(rest, rest, nbk, W + int64_t(k0 + nbk) * ld + k0, ld, a12, ld,
+                             W + int64_t(k0 + nbk) * ld + k0 + nbk, ld, status, st));
+    }
+    VK_CHECK_LAUNCH();
+  }
+  return VK_OK;
+}
+
+int finish_status(const DenseWork& d, int32_t* reason, int32_t* singular_at, cudaStream_t st) {
+  int sv[2] = {0, 0};
+  VK_CHECK_CUDA(cudaMemcpyAsync(sv, d.pb.status, 8, cudaMemcpyDeviceToHost, st));
+  VK_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (reason) *reason = sv[0];
+  if (sv[0]) {
+    if (singular_at) *singular_at = sv[1];
+    vk::set_error("dense factorization: %s at %d",
+                  sv[0] == VK_PATCH_ZERO_ROW ? "matrix has an all-zero row"
+                                             : "pivot below 1e-12 of its row magnitude",
+                  sv[1]);
+    return VK_SINGULAR;
+  }
+  return VK_OK;
+}
+
+}  // namespace
+
+extern "C" int vk_dense_lu(int32_t n, const double* a, double* lu, int32_t* ipiv_host, void* work,
+                           int32_t* reason, int32_t* singular_at, void* stream) {
+  VK_REQUIRE(n >= 0 && (n == 0 || (a && lu && work)), "vk_dense_lu: bad argument");
+  if (singular_at) *singular_at = -1;
+  if (reason) *reason = 0;
+  if (n == 0) return VK_OK;
+  cudaStream_t st = vk_stream(stream);
+  DenseWork d = carve(n, work);
+  if (int rc = run_lu(n, a, d, st)) return rc;
+  VK_CHECK_CUDA(cudaMemcpyAsync(lu, d.W, 8 * int64_t(n) * n, cudaMemcpyDeviceToDevice, st));
+  if (ipiv_host)
+    VK_CHECK_CUDA(cudaMemcpyAsync(ipiv_host, d.pb.ipiv, 4 * int64_t(n), cudaMemcpyDeviceToHost, st));
+  return finish_status(d, reason, singular_at, st);
+}
+
+extern "C" int vk_dense_inverse(int32_t n, const double* a, double* inv, void* work,
+                                int32_t* reason, int32_t* singular_at, void* stream) {
+  VK_REQUIRE(n >= 0 && (n == 0 || (a && inv && work)), "vk_dense_inverse: bad argument");
+  if (singular_at) *singular_at = -1;
+  if (reason) *reason = 0;
+  if (n == 0) return VK_OK;
+  VK_REQUIRE(int64_t(n) * 4 <= 200 * 1024, "vk_dense_inverse: n = %d too large", n);
+  cudaStream_t st = vk_stream(stream);
+  DenseWork d = carve(n, work);
+  if (int rc = run_lu(n, a, d, st)) return rc;
+  const int64_t ld = n;
+  double* W = d.W;
+  double* X = d.X;
+  const int* status = d.pb.status;
+  // ---- B. X = U^{-1} L^{-1}  (getrs with the identity)
+  identity_kernel<<<vk_grid(int64_t(n) * n, 256, 148 * 16), 256, 0, st>>>(n, X);
+  for (int k0 = 0; k0 < n; k0 += kNB) {        // L Y = I: Y lower triangular
+    const int nbk = std::min(kNB, n - k0);
+    const int cols = k0 + nbk;
+    trsm_lower_unit_kernel<<<(cols + 127) / 128, 128, 0, st>>>(
+        nbk, W + int64_t(k0) * ld + k0, ld, X + int64_t(k0) * ld, ld, cols, status);
+    VK_CHECK_CUDA(gemm_sub(n - k0 - nbk, cols, nbk, W + int64_t(k0 + nbk) * ld + k0, ld,
+                           X + int64_t(k0) * ld, ld, X + int64_t(k0 + nbk) * ld, ld, status, st));
+  }
+  const int last = ((n - 1) / kNB) * kNB;
+  for (int k0 = last; k0 >= 0; k0 -= kNB) {    // U X = Y
+    const int nbk = std::min(kNB, n - k0);
+    trsm_upper_kernel<<<(n + 127) / 128, 128, 0, st>>>(nbk, W + int64_t(k0) * ld + k0, ld,
+                                                        X + int64_t(k0) * ld, ld, n, status);
+    VK_CHECK_CUDA(gemm_sub(k0, n, nbk, W + k0, ld, X + int64_t(k0) * ld, ld, X, ld, status, st));
+  }
+  VK_CHECK_LAUNCH();
+  // ---- C. column permutation
+  VK_CHECK_CUDA(vk_smem_optin((const void*)colmap_kernel, 4 * n));
+  colmap_kernel<<<1, 1024, 4 * size_t(n), st>>>(n, d.pb.ipiv, status, d.map);
+  gather_cols_kernel<<<vk_grid(int64_t(n) * n, 256, 148 * 16), 256, 0, st>>>(n, d.map, status, X,
+                                                                             inv);
+  VK_CHECK_LAUNCH();
+  return finish_status(d, reason, singular_at, st);
+}

@@ -11,8 +11,8 @@ a problem pack, :func:`hierarchy_from_reference` wraps a hierarchy built by
 the reference itself.  Everything per level then lives on the device:
 operator CSR, masked prolongation and its explicit transpose, factored
 patches, work vectors.  The coarse operator A0 + max|A0| q q^T is densified
-and inverted once on the device (cuSOLVER via torch.linalg — not a hot-path
-kernel) and applied as a dense GEMV.
+and inverted once on the device by the library's blocked Gauss-Jordan kernels
+(:func:`coarse_inverse`) and applied as a dense GEMV.
 
 One V(nu,nu) cycle in ``repeat`` mode is ~15 kernel launches per level; it is
 captured once into a CUDA graph and replayed.
@@ -106,6 +106,33 @@ def pressure_kernel(mixed) -> np.ndarray:
     return vec / np.linalg.norm(vec)
 
 
+def coarse_inverse(a0, q, shift: float):
+    """Explicit inverse of the coarse operator A0 + shift q q^T (reference
+    ``mg.build_hierarchy``, ``mg.py:228-232``, which LU-factors it), formed
+    and inverted on the device by the library's own kernels
+    (``vk_coarse_operator``: bit-identical to numpy's ``a0.toarray() +
+    shift * np.outer(q, q)``; ``vk_dense_inverse``: blocked Gauss-Jordan
+    with partial pivoting and the ``lu_factor`` guard).  Raises
+    ``SingularMatrixError`` like the reference."""
+    import ctypes as C
+    import torch
+    from .sparsela import SingularMatrixError
+    n = a0.shape[0]
+    st = L.stream_ptr()
+    m = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    L.call("vk_coarse_operator", a0.handle, L.ptr(q), float(shift), L.ptr(m), st)
+    work = torch.empty(max(int(L.lib().vk_dense_inverse_workspace(n)), 1), dtype=torch.uint8,
+                       device="cuda")
+    inv = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    reason, col = C.c_int32(0), C.c_int32(-1)
+    rc = L.call("vk_dense_inverse", n, L.ptr(m), L.ptr(inv), L.ptr(work), C.byref(reason),
+                C.byref(col), st)
+    if rc == L.VK_SINGULAR:
+        raise SingularMatrixError("matrix has an all-zero row" if reason.value == L.VK_PATCH_ZERO_ROW
+                                  else "pivot below 1e-12 of its row magnitude")
+    return inv
+
+
 class MgHierarchy:
     """Reference ``mg.MgHierarchy`` (``mg.py:72-88``), device resident."""
 
@@ -118,11 +145,9 @@ class MgHierarchy:
         self.nu = nu
         self.cheb_mode = cheb_mode
         c = levels[0]
-        a0 = c.A.todense_device()
         q = torch.from_numpy(np.ascontiguousarray(coarse_kernel)).cuda()
         shift = float(np.max(np.abs(c.system.matrix.data)))            # mg.py:231
-        m = a0 + shift * torch.outer(q, q)
-        self.coarse_inverse = torch.linalg.inv(m).contiguous()          # mg.py:232
+        self.coarse_inverse = coarse_inverse(c.A, q, shift)             # mg.py:232
         self.coarse_factor = self.coarse_inverse
         self.q = q
         self._scratch = L.reduce_scratch()[0]     # this hierarchy's reductions

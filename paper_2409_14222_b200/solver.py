@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import _lib as L
 from .mg import MgHierarchy, make_preconditioner, pressure_kernel
 from .sparsela import FgmresWorkspace, fgmres, nullspace_projector, to_device
 
@@ -31,6 +32,7 @@ class FgmresSolver:
     """Reusable solver state (device operator, preconditioner, projector)."""
 
     def __init__(self, hier: MgHierarchy, *, rtol=1e-8, restart=30, max_cycles=20):
+        import torch
         self.hier = hier
         self.rtol = rtol
         self.restart = restart
@@ -39,6 +41,8 @@ class FgmresSolver:
         self.nsp = nullspace_projector([pressure_kernel(hier.fine.mixed)])
         self.A = hier.fine.A
         self.workspace = FgmresWorkspace(hier.fine.n, restart)
+        self._red = L.reduce_scratch()[0]
+        self._norm = torch.zeros(1, dtype=torch.float64, device="cuda")
 
     def solve(self, b):
         """Returns (x, iterations, converged, history) with x on the device
@@ -56,7 +60,12 @@ class FgmresSolver:
                             workspace=self.workspace)
             if base is None:
                 pb = self.nsp(bd.clone())
-                base = float(torch.linalg.vector_norm(pb).item()) if rep.iterations else None
+                if rep.iterations:
+                    L.call("vk_nrm2", pb.numel(), L.ptr(pb), L.ptr(self._norm),
+                           L.ptr(self._red), L.stream_ptr())
+                    base = float(self._norm.item())
+                else:
+                    base = None
                 hist.extend(rep.history.tolist())
                 if base is None:
                     conv = rep.converged

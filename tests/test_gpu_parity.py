@@ -17,11 +17,16 @@ pytestmark = pytest.mark.gpu
 ALL = ["cfg1"] + SMALL_MG + FULL_MG
 REL_SWEEP = 1e-10
 REL_HIST = 1e-10
-# The reference's own histories move by `floor` when only its coarse getrf
-# runs on 8 BLAS threads instead of 1 (tools/reference_selfvar.py,
-# tests/golden/reference_selfvar.json): the history gate is
-# max(1e-10, SELFVAR_FACTOR * floor); the strict 1e-10 verdict is printed.
-SELFVAR_FACTOR = 4.0
+# History gate.  cfg2/cfg3/cfg4 (BASELINE configs): the strict 1e-10.  cfg5
+# and the small cases: the reference's own floor — the largest history change
+# the reference shows when only its coarse solve is replaced by another valid
+# factorization (getrf on 2/4/8 BLAS threads, the getri inverse, an exact
+# solve; tools/reference_selfvar.py, tests/golden/reference_selfvar.json)
+# if that is above 1e-10.  tests/test_gpu_coarse_diag.py shows that with the
+# reference's own coarse solve swapped in, the device path is inside 1e-10
+# on these cases too: the coarse LU's cond * eps is the whole gap
+# (DESIGN.md §2).
+STRICT_HIST = ("cfg2", "cfg3", "cfg4")
 
 
 def history_floor(name):
@@ -173,11 +178,11 @@ def test_mg_fgmres_history(name, capsys):
     m = min(len(hist), len(hist_ref))
     rel = np.max(np.abs(hist[:m] - hist_ref[:m]) / hist_ref[:m])
     floor = history_floor(name)
-    tol = max(REL_HIST, SELFVAR_FACTOR * floor)
+    tol = REL_HIST if name in STRICT_HIST else max(REL_HIST, floor)
     with capsys.disabled():
         print(f"\n[{name}] iterations {its} (ref {its_ref}) max history rel diff {rel:.3e} "
               f"(strict gate 1e-10: {'pass' if rel <= REL_HIST else 'FAIL'}; reference "
-              f"self-variation {floor:.2e}; test tolerance {tol:.2e})")
+              f"floor {floor:.2e}; test tolerance {tol:.2e})")
     assert conv
     assert abs(its - its_ref) <= 1
     assert rel <= tol, rel
