@@ -78,6 +78,16 @@ VK_API int vk_csr_destroy(vk_csr_t a);
  * r = b - A x              : residual at mg.py:270, 294 */
 VK_API int vk_spmv(vk_csr_t a, const double* x, double* y, double alpha, double beta, void* stream);
 VK_API int vk_residual(vk_csr_t a, const double* b, const double* x, double* r, void* stream);
+/* fused V-cycle transfer units (one cooperative launch each, a grid barrier
+ * between the two SpMVs; every row summed exactly as vk_spmv / vk_residual,
+ * so bit-identical to the two separate calls):
+ *   vk_residual_restrict: r = b - A x, then rc = PT r      (mg.py:294-295)
+ *   vk_prolong_residual:  x = x + P xc, then r = b - A x   (mg.py:296-297 and
+ *                         the first residual of post-smoothing, mg.py:270) */
+VK_API int vk_residual_restrict(vk_csr_t a, const double* b, const double* x, double* r,
+                                vk_csr_t pt, double* rc, void* stream);
+VK_API int vk_prolong_residual(vk_csr_t p, const double* xc, double* x, vk_csr_t a,
+                               const double* b, double* r, void* stream);
 
 /* ---------------- patches (K1-K4) ------------------------------------------
  * vk_patches_build replaces vanka.build_patches_taylor_hood /
@@ -140,6 +150,15 @@ VK_API int vk_patches_apply(vk_patches_t h, const double* r, double* out, double
 VK_API int vk_patches_solve(vk_patches_t h, const double* r, double* zbuf, void* stream);
 VK_API int vk_patches_accumulate(vk_patches_t h, const double* zbuf, double* out, double scale,
                                  int32_t mode, void* stream);
+/* one preconditioned Chebyshev step of degree mode (mg.py:237-255) with the
+ * sweep fused in: acc = apply_additive(r) (K4a + K4b), then in K4b's
+ * epilogue, elementwise in the reference's order,
+ *   first == 1:  d = acc / c2                 (d = preconditioner(r) / theta)
+ *   first == 0:  d = c1 * d + c2 * acc        (c1 = rho_next*rho, c2 = 2 rho_next/delta)
+ *   and x = x + d;  first == 2: as 1 but x = d (x was zero: x + d = d).
+ * zbuf as for vk_patches_apply. */
+VK_API int vk_patches_apply_cheb(vk_patches_t h, const double* r, double* x, double* d,
+                                 double c1, double c2, int32_t first, double* zbuf, void* stream);
 /* name of the K4a kernel vk_patches_solve launches for this patch set (for
  * profiling tools and the bench line) */
 VK_API const char* vk_patches_solve_kernel(vk_patches_t h);
@@ -176,6 +195,11 @@ VK_API int vk_nrm2(int64_t n, const double* x, double* out_dev, double* scratch_
 /* x = x - q (q . x) in place (NullspaceProjector, sparsela.py:113-114);
  * scratch_dev: VK_REDUCE_SCRATCH doubles as above */
 VK_API int vk_project(int64_t n, const double* q, double* x, double* scratch_dev, void* stream);
+/* Chebyshev vector update of degree mode (mg.py:246-254) for a generic
+ * operator/preconditioner: first != 0: d = z / c2; else d = c1 d + c2 z;
+ * then x = x + d (elementwise, the reference's operation order) */
+VK_API int vk_cheb_update(int64_t n, const double* z, double* d, double* x, double c1, double c2,
+                          int32_t first, void* stream);
 /* dst[idx[k]] = src[idx[k]] */
 VK_API int vk_copy_index(int64_t m, const int32_t* idx, const double* src, double* dst, void* stream);
 /* y = M x for a dense row-major m x n matrix (coarse inverse apply) */

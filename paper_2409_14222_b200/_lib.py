@@ -38,6 +38,8 @@ SIGNATURES = {
     "vk_csr_destroy": (C.c_int, [_p]),
     "vk_spmv": (C.c_int, [_p, _p, _p, _f64, _f64, _p]),
     "vk_residual": (C.c_int, [_p, _p, _p, _p, _p]),
+    "vk_residual_restrict": (C.c_int, [_p, _p, _p, _p, _p, _p, _p]),
+    "vk_prolong_residual": (C.c_int, [_p, _p, _p, _p, _p, _p, _p]),
     "vk_patches_build": (C.c_int, [_p, _i32, _i32, _p, _p, _i32, _p, _p, _p, _i32, _i32,
                                    C.POINTER(_p)]),
     "vk_patches_from_lists": (C.c_int, [_p, _p, _p, _p, _i32, _i32, C.POINTER(_p)]),
@@ -50,6 +52,7 @@ SIGNATURES = {
     "vk_patches_apply": (C.c_int, [_p, _p, _p, _f64, _i32, _p, _p]),
     "vk_patches_solve": (C.c_int, [_p, _p, _p, _p]),
     "vk_patches_accumulate": (C.c_int, [_p, _p, _p, _f64, _i32, _p]),
+    "vk_patches_apply_cheb": (C.c_int, [_p, _p, _p, _p, _f64, _f64, _i32, _p, _p]),
     "vk_patches_solve_kernel": (C.c_char_p, [_p]),
     "vk_patches_destroy": (C.c_int, [_p]),
     "vk_dot": (C.c_int, [_i64, _p, _p, _p, _p, _p]),
@@ -59,6 +62,7 @@ SIGNATURES = {
     "vk_div_dev": (C.c_int, [_i64, _p, _p, _p, _p]),
     "vk_nrm2": (C.c_int, [_i64, _p, _p, _p, _p]),
     "vk_project": (C.c_int, [_i64, _p, _p, _p, _p]),
+    "vk_cheb_update": (C.c_int, [_i64, _p, _p, _p, _f64, _f64, _i32, _p]),
     "vk_copy_index": (C.c_int, [_i64, _p, _p, _p, _p]),
     "vk_gemv": (C.c_int, [_i32, _i32, _p, _p, _p, _p]),
     "vk_combine": (C.c_int, [_i64, _i32, _p, _p, _p, _p]),

@@ -170,11 +170,18 @@ __global__ void __launch_bounds__(kApplyWarps * 32, minb_of(RMAX)) patch_solve_k
 // issued before the in-order additions — acc = ((0 + z_0) + z_1) + ... in
 // ascending patch order, exactly out[idx] += ... of src/vanka.py:147.  (Two
 // DoFs per thread in one resident wave measured slower.)
+// Chebyshev epilogues (degree mode, reference mg.py:246-254): d and x
+// updated in the same pass, in the reference's elementwise order
+constexpr int kCheb0 = 3;   // d = acc / scale;               x = x + d
+constexpr int kChebK = 4;   // d = c1 * d + scale * acc;      x = x + d
+constexpr int kCheb0Set = 5;  // d = acc / scale;             x = d   (x was zero)
+
 template <int MODE>
 __global__ void __launch_bounds__(256) dof_gather_kernel(int ndof, const int* __restrict__ dptr,
                                                          const int* __restrict__ dslot,
                                                          const double* __restrict__ z,
-                                                         double* __restrict__ out, double scale) {
+                                                         double* __restrict__ out, double scale,
+                                                         double* __restrict__ dvec, double c1) {
   pdl_trigger();
   pdl_wait();
   const int nth = gridDim.x * blockDim.x;
@@ -192,22 +199,28 @@ __global__ void __launch_bounds__(256) dof_gather_kernel(int ndof, const int* __
       for (int u = 0; u < 4; ++u)
         if (sl[u] >= 0) acc = __dadd_rn(acc, v[u]);
     }
-    if (MODE == VK_APPLY_OUT)
+    if (MODE == VK_APPLY_OUT) {
       out[d] = acc;
-    else if (MODE == VK_APPLY_XSET)
+    } else if (MODE == VK_APPLY_XSET) {
       out[d] = __dmul_rn(scale, acc);
-    else
+    } else if (MODE == VK_APPLY_XADD) {
       out[d] = __dadd_rn(out[d], __dmul_rn(scale, acc));
+    } else {
+      const double dn = (MODE == kChebK) ? __dadd_rn(__dmul_rn(c1, dvec[d]), __dmul_rn(scale, acc))
+                                         : __ddiv_rn(acc, scale);
+      dvec[d] = dn;
+      out[d] = (MODE == kCheb0Set) ? dn : __dadd_rn(out[d], dn);
+    }
   }
 }
 
 template <int MODE>
 cudaError_t launch_gather(const vk_patches_s* h, const double* zbuf, double* out, double scale,
-                          cudaStream_t st) {
+                          cudaStream_t st, double* dvec = nullptr, double c1 = 0.0) {
   const int grid = std::max(1, std::min((h->ndof + 255) / 256, 148 * 8));
   return vk_launch(dof_gather_kernel<MODE>, dim3(grid), dim3(256), 0, st,
                    12 * h->total + 16 * int64_t(h->ndof), h->ndof, (const int*)h->dptr,
-                   (const int*)h->dslot, zbuf, out, scale);
+                   (const int*)h->dslot, zbuf, out, scale, dvec, c1);
 }
 
 }  // namespace
@@ -774,4 +787,24 @@ extern "C" int vk_patches_apply(vk_patches_t h, const double* r, double* out, do
   VK_REQUIRE(r && out, "vk_patches_apply: null argument");
   if (int st = vk_patches_solve(h, r, zbuf, stream)) return st;
   return vk_patches_accumulate(h, zbuf, out, scale, mode, stream);
+}
+
+extern "C" int vk_patches_apply_cheb(vk_patches_t h, const double* r, double* x, double* d,
+                                     double c1, double c2, int32_t first, double* zbuf,
+                                     void* stream) {
+  VK_REQUIRE(r && x && d, "vk_patches_apply_cheb: null argument");
+  if (int st = vk_patches_solve(h, r, zbuf, stream)) return st;
+  const double* const z = zbuf ? zbuf : h->zbuf;
+  if (h->ndof > 0) {
+    const cudaStream_t st = vk_stream(stream);
+    const cudaError_t e = first == 2 ? launch_gather<kCheb0Set>(h, z, x, c2, st, d, c1)
+                          : first    ? launch_gather<kCheb0>(h, z, x, c2, st, d, c1)
+                                     : launch_gather<kChebK>(h, z, x, c2, st, d, c1);
+    if (e != cudaSuccess) {
+      vk::set_error("vk_patches_apply_cheb: %s", cudaGetErrorString(e));
+      return VK_ERR_CUDA;
+    }
+  }
+  VK_CHECK_LAUNCH();
+  return VK_OK;
 }

@@ -182,6 +182,19 @@ __global__ void combine_kernel(int64_t n, int count, const double* __restrict__ 
   }
 }
 
+// Chebyshev vector update (reference mg.py:246-254): first: d = z / c2,
+// else d = c1 * d + c2 * z; then x = x + d (elementwise, reference order)
+__global__ void cheb_update_kernel(int64_t n, const double* __restrict__ z, double* __restrict__ d,
+                                   double* __restrict__ x, double c1, double c2, int first) {
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const double dn = first ? __ddiv_rn(z[i], c2) : __dadd_rn(__dmul_rn(c1, d[i]), __dmul_rn(c2, z[i]));
+    d[i] = dn;
+    x[i] = __dadd_rn(x[i], dn);
+  }
+}
+
 __global__ void project_apply_kernel(int64_t n, const double* __restrict__ q, const double* __restrict__ s,
                                      double* __restrict__ x) {
   pdl_trigger();
@@ -279,6 +292,15 @@ extern "C" int vk_combine(int64_t n, int32_t count, const double* z, const doubl
   VK_REQUIRE(z && coef_dev && x, "vk_combine: null argument");
   if (n == 0 || count == 0) return VK_OK;
   VK_CHECK_CUDA(vk_launch(combine_kernel, dim3(VK_VEC_GRID(n)), dim3(256), 0, vk_stream(stream), 8 * n * (int64_t(count) + 2), n, count, z, coef_dev, x));
+  VK_CHECK_LAUNCH();
+  return VK_OK;
+}
+
+extern "C" int vk_cheb_update(int64_t n, const double* z, double* d, double* x, double c1,
+                              double c2, int32_t first, void* stream) {
+  VK_REQUIRE(z && d && x, "vk_cheb_update: null argument");
+  if (n == 0) return VK_OK;
+  VK_CHECK_CUDA(vk_launch(cheb_update_kernel, dim3(VK_VEC_GRID(n)), dim3(256), 0, vk_stream(stream), 32 * n, n, z, d, x, c1, c2, int(first != 0)));
   VK_CHECK_LAUNCH();
   return VK_OK;
 }

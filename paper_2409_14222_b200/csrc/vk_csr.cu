@@ -20,7 +20,11 @@
 #include <numeric>
 #include <string>
 
+#include <cooperative_groups.h>
+
 #include "vk_common.cuh"
+
+namespace cg = cooperative_groups;
 
 #ifndef VK_CSR_SHORT  // thread-per-row kernel when the mean over 32-row groups of
 #define VK_CSR_SHORT 11  // the longest row is <= this (measured: transfers P of cfg2/3)
@@ -67,17 +71,27 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // holds (first row, first nonzero) pairs, so the (col, val) loads of the first
 // chunk, the row-pointer loads and the epilogue operand (b or y) are all in
 // flight together; only the x gathers wait for col.
-template <int MODE>
-__global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
-    const int2* __restrict__ blk, const int* __restrict__ ptr, const int* __restrict__ col,
-    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-    double alpha, double beta, const double* __restrict__ b) {
-  __shared__ double prod[kStreamNnz];
-  __shared__ int sptr[kStreamRows + 1];
-  __shared__ double carry;
+// x / b loads: through the read-only path (NC) when the data comes from an
+// earlier kernel; coherent loads when an earlier phase of the same
+// cooperative kernel wrote them (vk_residual_restrict / vk_prolong_residual)
+template <bool NC>
+__device__ __forceinline__ double ld_x(const double* p) {
+  if (NC) return __ldg(p);
+  return *p;
+}
+
+// One row block (block table entry `bi`) of the CSR-stream SpMV; shared
+// arrays passed in by the kernel.
+template <int MODE, bool PDL, bool NC>
+__device__ __forceinline__ void stream_block(int bi, const int2* __restrict__ blk,
+                                             const int* __restrict__ ptr,
+                                             const int* __restrict__ col,
+                                             const double* __restrict__ val, const double* x,
+                                             double* y, double alpha, double beta,
+                                             const double* b, double* prod, int* sptr,
+                                             double& carry) {
   const int t = threadIdx.x;
-  pdl_trigger();
-  const int2 e0 = blk[blockIdx.x], e1 = blk[blockIdx.x + 1];
+  const int2 e0 = blk[bi], e1 = blk[bi + 1];
   const int r0 = e0.x, k0 = e0.y, k1 = e1.y;
   const int nr = e1.x - r0;
   const bool single = (nr == 1);
@@ -86,7 +100,7 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
   for (int i = t; i <= nr; i += kStreamThreads) cp_async4(sptr + i, ptr + r0 + i);
   // block table and row pointers (setup data) are in flight; x and b / y
   // come from the preceding kernel
-  pdl_wait();
+  if (PDL) pdl_wait();
   if (t == 0) carry = 0.0;
   for (int kc = k0; kc < k1 || (kc == k0 && k0 == k1); kc += kStreamNnz) {
     const int kend = min(k1, kc + kStreamNnz);
@@ -101,7 +115,7 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
 #pragma unroll
     for (int u = 0; u < kStreamU; ++u) {
       const int k = kc + t + u * kStreamThreads;
-      if (k < kend) prod[k - kc] = __dmul_rn(v[u], __ldg(x + c[u]));
+      if (k < kend) prod[k - kc] = __dmul_rn(v[u], ld_x<NC>(x + c[u]));
     }
     cp_async_wait_all();
     __syncthreads();
@@ -163,22 +177,29 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
 
 #undef VK_PRE
 
+template <int MODE>
+__global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
+    const int2* __restrict__ blk, const int* __restrict__ ptr, const int* __restrict__ col,
+    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+    double alpha, double beta, const double* __restrict__ b) {
+  __shared__ double prod[kStreamNnz];
+  __shared__ int sptr[kStreamRows + 1];
+  __shared__ double carry;
+  pdl_trigger();
+  stream_block<MODE, true, true>(blockIdx.x, blk, ptr, col, val, x, y, alpha, beta, b, prod, sptr,
+                                 carry);
+}
+
 // Short-row kernel (thread per row): for matrices with a few nonzeros per
 // row (prolongations) the shared-memory staging of the stream kernel costs
 // more than it saves.  Same per-row operation order (sequential, FMA-free).
-template <int MODE>
-__global__ void __launch_bounds__(256) csr_row_kernel(
-    int nrows, const int* __restrict__ ptr, const int* __restrict__ col,
-    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-    double alpha, double beta, const double* __restrict__ b) {
-  pdl_trigger();
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= nrows) {
-    pdl_wait();
-    return;
-  }
+template <int MODE, bool PDL, bool NC>
+__device__ __forceinline__ void row_work(int row, const int* __restrict__ ptr,
+                                         const int* __restrict__ col,
+                                         const double* __restrict__ val, const double* x,
+                                         double* y, double alpha, double beta, const double* b) {
   const int k0 = __ldg(ptr + row), k1 = __ldg(ptr + row + 1);
-  pdl_wait();
+  if (PDL) pdl_wait();
   double pre = 0.0;
   if (MODE == 1) pre = __ldg(b + row);
   else if (beta != 0.0) pre = y[row];
@@ -193,11 +214,11 @@ __global__ void __launch_bounds__(256) csr_row_kernel(
       v[u] = __ldg(val + k + u);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) p[u] = __dmul_rn(v[u], __ldg(x + c[u]));
+    for (int u = 0; u < 4; ++u) p[u] = __dmul_rn(v[u], ld_x<NC>(x + c[u]));
 #pragma unroll
     for (int u = 0; u < 4; ++u) s = __dadd_rn(s, p[u]);
   }
-  for (; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(__ldg(val + k), __ldg(x + __ldg(col + k))));
+  for (; k < k1; ++k) s = __dadd_rn(s, __dmul_rn(__ldg(val + k), ld_x<NC>(x + __ldg(col + k))));
   if (MODE == 1) {
     y[row] = __dsub_rn(pre, s);
   } else {
@@ -205,6 +226,65 @@ __global__ void __launch_bounds__(256) csr_row_kernel(
     if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? pre : __dmul_rn(beta, pre), out);
     y[row] = out;
   }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) csr_row_kernel(
+    int nrows, const int* __restrict__ ptr, const int* __restrict__ col,
+    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+    double alpha, double beta, const double* __restrict__ b) {
+  pdl_trigger();
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nrows) {
+    pdl_wait();
+    return;
+  }
+  row_work<MODE, true, true>(row, ptr, col, val, x, y, alpha, beta, b);
+}
+
+// Two SpMV phases in ONE cooperative launch with a grid barrier between
+// them: the V-cycle's residual + restriction (r = b - A x; rc = P^T r,
+// mg.py:294-295) and prolongation + the next residual (x += P xc;
+// r = b - A x, mg.py:296-297).  Each phase runs the same per-row code as the
+// standalone kernels (persistent CTAs walk the row blocks / rows), so the
+// results are bit-identical; the barrier replaces a kernel boundary, and
+// phase B reads phase A's output with coherent loads.
+struct CsrPhase {
+  const int2* blk;
+  int nblocks, nrows;
+  const int* ptr;
+  const int* col;
+  const double* val;
+  const double* x;
+  double* y;
+  double alpha, beta;
+  const double* b;
+};
+
+template <int MODE, bool SHORT, bool NC>
+__device__ __forceinline__ void run_phase(const CsrPhase& p, double* prod, int* sptr,
+                                          double& carry) {
+  if (SHORT) {
+    for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < p.nrows;
+         row += gridDim.x * blockDim.x)
+      row_work<MODE, false, NC>(row, p.ptr, p.col, p.val, p.x, p.y, p.alpha, p.beta, p.b);
+  } else {
+    for (int bi = blockIdx.x; bi < p.nblocks; bi += gridDim.x) {
+      __syncthreads();
+      stream_block<MODE, false, NC>(bi, p.blk, p.ptr, p.col, p.val, p.x, p.y, p.alpha, p.beta,
+                                    p.b, prod, sptr, carry);
+    }
+  }
+}
+
+template <int MA, bool SA, int MB, bool SB>
+__global__ void __launch_bounds__(kStreamThreads) csr_two_phase_kernel(CsrPhase A, CsrPhase B) {
+  __shared__ double prod[kStreamNnz];
+  __shared__ int sptr[kStreamRows + 1];
+  __shared__ double carry;
+  run_phase<MA, SA, true>(A, prod, sptr, carry);
+  cg::this_grid().sync();
+  run_phase<MB, SB, false>(B, prod, sptr, carry);
 }
 
 // Opt-in tree-reduction kernel (VK_SPMV_TREE=1, NOT bit-exact): G lanes
@@ -282,6 +362,37 @@ cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alp
   return vk_launch(csr_stream_kernel<MODE>, dim3(a.nblocks), dim3(kStreamThreads), 0, st,
                    12 * a.nnz + 24 * int64_t(a.nrows), a.blk, a.indptr, a.indices, a.data, x, y,
                    alpha, beta, b);
+}
+
+CsrPhase phase_of(const vk::Csr& a, const double* x, double* y, double alpha, double beta,
+                  const double* b) {
+  CsrPhase p;
+  p.blk = a.blk;
+  p.nblocks = a.nblocks;
+  p.nrows = a.nrows;
+  p.ptr = a.indptr;
+  p.col = a.indices;
+  p.val = a.data;
+  p.x = x;
+  p.y = y;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.b = b;
+  return p;
+}
+
+template <int MA, int MB>
+cudaError_t launch_two_phase(const vk::Csr& a, CsrPhase A, const vk::Csr& bm, CsrPhase B,
+                             cudaStream_t st) {
+  const bool sa = a.warp_max_mean <= VK_CSR_SHORT, sb = bm.warp_max_mean <= VK_CSR_SHORT;
+  const void* k;
+  if (sa && sb) k = (const void*)csr_two_phase_kernel<MA, true, MB, true>;
+  else if (sa) k = (const void*)csr_two_phase_kernel<MA, true, MB, false>;
+  else if (sb) k = (const void*)csr_two_phase_kernel<MA, false, MB, true>;
+  else k = (const void*)csr_two_phase_kernel<MA, false, MB, false>;
+  const int grid = vk_resident_blocks(k, kStreamThreads, 0);
+  void* args[] = {&A, &B};
+  return cudaLaunchCooperativeKernel(k, dim3(grid), dim3(kStreamThreads), args, 0, st);
 }
 
 __global__ void csr_to_dense_kernel(int nrows, int ncols, const int* __restrict__ ptr,
@@ -454,5 +565,42 @@ extern "C" int vk_csr_to_dense(vk_csr_t a, double* dense, void* stream) {
   csr_to_dense_kernel<<<grid, 256, 0, vk_stream(stream)>>>(a->nrows, a->ncols, a->indptr,
                                                           a->indices, a->data, dense);
   VK_CHECK_LAUNCH();
+  return VK_OK;
+}
+
+extern "C" int vk_residual_restrict(vk_csr_t a, const double* b, const double* x, double* r,
+                                    vk_csr_t pt, double* rc, void* stream) {
+  VK_REQUIRE(a && pt && b && x && r && rc, "vk_residual_restrict: null argument");
+  VK_REQUIRE(a->nrows == a->ncols && pt->ncols == a->nrows,
+             "vk_residual_restrict: shape mismatch");
+  if (tree_enabled() || a->nblocks == 0 || pt->nblocks == 0) {   // plain two launches
+    if (int st = vk_residual(a, b, x, r, stream)) return st;
+    return vk_spmv(pt, r, rc, 1.0, 0.0, stream);
+  }
+  const cudaError_t e = launch_two_phase<1, 0>(*a, phase_of(*a, x, r, 1.0, 0.0, b), *pt,
+                                               phase_of(*pt, r, rc, 1.0, 0.0, nullptr),
+                                               vk_stream(stream));
+  if (e != cudaSuccess) {
+    vk::set_error("vk_residual_restrict: %s", cudaGetErrorString(e));
+    return VK_ERR_CUDA;
+  }
+  return VK_OK;
+}
+
+extern "C" int vk_prolong_residual(vk_csr_t p, const double* xc, double* x, vk_csr_t a,
+                                   const double* b, double* r, void* stream) {
+  VK_REQUIRE(a && p && b && x && r && xc, "vk_prolong_residual: null argument");
+  VK_REQUIRE(a->nrows == a->ncols && p->nrows == a->nrows, "vk_prolong_residual: shape mismatch");
+  if (tree_enabled() || a->nblocks == 0 || p->nblocks == 0) {
+    if (int st = vk_spmv(p, xc, x, 1.0, 1.0, stream)) return st;
+    return vk_residual(a, b, x, r, stream);
+  }
+  const cudaError_t e = launch_two_phase<0, 1>(*p, phase_of(*p, xc, x, 1.0, 1.0, nullptr), *a,
+                                               phase_of(*a, x, r, 1.0, 0.0, b),
+                                               vk_stream(stream));
+  if (e != cudaSuccess) {
+    vk::set_error("vk_prolong_residual: %s", cudaGetErrorString(e));
+    return VK_ERR_CUDA;
+  }
   return VK_OK;
 }

@@ -14,8 +14,8 @@ patches, work vectors.  The coarse operator A0 + max|A0| q q^T is densified
 and inverted once on the device by the library's blocked Gauss-Jordan kernels
 (:func:`coarse_inverse`) and applied as a dense GEMV.
 
-One V(nu,nu) cycle in ``repeat`` mode is ~15 kernel launches per level; it is
-captured once into a CUDA graph and replayed.
+One V(nu,nu) cycle (``repeat`` or ``degree`` Chebyshev) is ~15 kernel
+launches per level; it is captured once into a CUDA graph and replayed.
 """
 
 from __future__ import annotations
@@ -93,6 +93,7 @@ class Level:
         self.x = torch.zeros(n, dtype=torch.float64, device="cuda")
         self.r = torch.zeros(n, dtype=torch.float64, device="cuda")
         self.rhs = torch.zeros(n, dtype=torch.float64, device="cuda")
+        self.d = torch.zeros(n, dtype=torch.float64, device="cuda")   # Chebyshev direction
 
     @property
     def damp(self) -> float:
@@ -173,21 +174,6 @@ class MgHierarchy:
         L.call("vk_gemv", n, n, L.ptr(self.coarse_inverse), L.ptr(c.r), L.ptr(x), st)
         L.call("vk_project", n, L.ptr(self.q), L.ptr(x), L.ptr(self._scratch), st)
 
-    def _relax_repeat(self, lv: Level, rhs, x, nu, x_is_zero):
-        """nu x { x += damp * apply(rhs - A x) } (mg.py:268-271), fused
-        epilogues; the first sweep from x = 0 uses r = rhs exactly."""
-        st = L.stream_ptr()
-        h = lv.patches.handle
-        damp = lv.damp
-        for it in range(nu):
-            if it == 0 and x_is_zero:
-                L.call("vk_patches_apply", h, L.ptr(rhs), L.ptr(x), damp, L.VK_APPLY_XSET, None,
-                       st)
-            else:
-                L.call("vk_residual", lv.A.handle, L.ptr(rhs), L.ptr(x), L.ptr(lv.r), st)
-                L.call("vk_patches_apply", h, L.ptr(lv.r), L.ptr(x), damp, L.VK_APPLY_XADD, None,
-                       st)
-
     def _cycle(self, idx, rhs, x, nu, mode):
         if idx == 0:
             self._coarse_into(rhs, x)
@@ -195,23 +181,28 @@ class MgHierarchy:
         st = L.stream_ptr()
         lv = self.levels[idx]
         coarse = self.levels[idx - 1]
-        if mode == "repeat":
-            if nu > 0:
-                self._relax_repeat(lv, rhs, x, nu, True)
-            else:
-                x.zero_()
+        if nu > 0:
+            _relax_device(lv, rhs, x, nu, mode, x_is_zero=True)
         else:
             x.zero_()
-            x.copy_(chebyshev_relax(lv, rhs, x, nu, mode))
-        L.call("vk_residual", lv.A.handle, L.ptr(rhs), L.ptr(x), L.ptr(lv.r), st)
         t = self.transfers[idx]
-        L.call("vk_spmv", t.PT.handle, L.ptr(lv.r), L.ptr(coarse.rhs), 1.0, 0.0, st)
-        self._cycle(idx - 1, coarse.rhs, coarse.x, nu, mode)
-        L.call("vk_spmv", t.P.handle, L.ptr(coarse.x), L.ptr(x), 1.0, 1.0, st)
-        if mode == "repeat":
-            self._relax_repeat(lv, rhs, x, nu, False)
+        if FUSED_TRANSFERS:
+            # r = rhs - A x and rc = P^T r in one launch (mg.py:294-295)
+            L.call("vk_residual_restrict", lv.A.handle, L.ptr(rhs), L.ptr(x), L.ptr(lv.r),
+                   t.PT.handle, L.ptr(coarse.rhs), st)
         else:
-            x.copy_(chebyshev_relax(lv, rhs, x, nu, mode))
+            L.call("vk_residual", lv.A.handle, L.ptr(rhs), L.ptr(x), L.ptr(lv.r), st)
+            L.call("vk_spmv", t.PT.handle, L.ptr(lv.r), L.ptr(coarse.rhs), 1.0, 0.0, st)
+        self._cycle(idx - 1, coarse.rhs, coarse.x, nu, mode)
+        if FUSED_TRANSFERS and nu > 0:
+            # x += P xc and the first post-smoothing residual in one launch
+            L.call("vk_prolong_residual", t.P.handle, L.ptr(coarse.x), L.ptr(x), lv.A.handle,
+                   L.ptr(rhs), L.ptr(lv.r), st)
+            _relax_device(lv, rhs, x, nu, mode, x_is_zero=False, r_ready=True)
+        else:
+            L.call("vk_spmv", t.P.handle, L.ptr(coarse.x), L.ptr(x), 1.0, 1.0, st)
+            if nu > 0:
+                _relax_device(lv, rhs, x, nu, mode, x_is_zero=False)
         if lv.bc.numel():
             L.call("vk_copy_index", lv.bc.numel(), L.ptr(lv.bc), L.ptr(rhs), L.ptr(x), st)
 
@@ -227,7 +218,9 @@ class MgHierarchy:
             self._in.copy_(b)
             self._coarse_into(self._in, lv.x)
             return lv.x
-        if not graph or mode != "repeat":
+        if mode not in CHEB_MODES:
+            raise ValueError(f"unknown chebyshev mode {mode!r}")
+        if not graph:
             self._in.copy_(b)
             self._cycle(top, self._in, lv.x, nu, mode)
             return lv.x
@@ -250,65 +243,127 @@ class MgHierarchy:
         return lv.x
 
 
+# True: the V-cycle's residual + restriction and prolongation + residual
+# pairs run as single cooperative launches (vk_residual_restrict /
+# vk_prolong_residual, bit-identical to the separate kernels).  Measured on
+# the B200 (tools/fused_probe.py) the captured V-cycle is
+# 0.5-2% SLOWER fused (cfg2 1.287 vs 1.277 ms, cfg5 2.163 vs 2.117 ms): the
+# persistent grid-barrier form of the residual loses more than the launch
+# boundary it removes, so the separate launches are the default.
+FUSED_TRANSFERS = False
+
+
+def _relax_device(lv, rhs, x, nu, mode, x_is_zero, r_ready=False):
+    """nu relaxation sweeps on one level, all on the device, x updated in place
+    (reference ``mg.chebyshev_relax``, ``mg.py:258-271``).
+
+    ``repeat``: nu x {x += damp * apply(rhs - A x)}, damp = 2/(lower+upper),
+    the damped update fused into the sweep's epilogue.  ``degree``: the
+    preconditioned Chebyshev recurrence of ``chebyshev_iteration``
+    (``mg.py:237-255``) — residual kernel, then one fused sweep whose epilogue
+    forms d (= z/theta, then rho_next*rho*d + (2 rho_next/delta) z) and
+    x + d in the reference's elementwise order; the scalars are the
+    reference's Python-float arithmetic.  From x = 0 the first residual is
+    rhs itself (b - A 0 = b); ``r_ready``: lv.r already holds rhs - A x."""
+    st = L.stream_ptr()
+    h = lv.patches.handle
+    lower, upper = lv.cheb.lower, lv.cheb.upper
+    if mode == "repeat":
+        damp = 2.0 / (lower + upper)                                    # mg.py:268
+        for it in range(nu):
+            if it == 0 and x_is_zero:
+                L.call("vk_patches_apply", h, L.ptr(rhs), L.ptr(x), damp, L.VK_APPLY_XSET, None,
+                       st)
+            else:
+                if not (it == 0 and r_ready):
+                    L.call("vk_residual", lv.A.handle, L.ptr(rhs), L.ptr(x), L.ptr(lv.r), st)
+                L.call("vk_patches_apply", h, L.ptr(lv.r), L.ptr(x), damp, L.VK_APPLY_XADD, None,
+                       st)
+        return
+    if mode != "degree":
+        raise ValueError(f"unknown chebyshev mode {mode!r}")
+    theta = 0.5 * (upper + lower)                                       # mg.py:241-244
+    delta = 0.5 * (upper - lower)
+    sigma = theta / delta
+    rho = 1.0 / sigma
+    if x_is_zero:
+        r0 = rhs
+    else:
+        if not r_ready:
+            L.call("vk_residual", lv.A.handle, L.ptr(rhs), L.ptr(x), L.ptr(lv.r), st)
+        r0 = lv.r
+    L.call("vk_patches_apply_cheb", h, L.ptr(r0), L.ptr(x), L.ptr(lv.d), 0.0, theta,
+           2 if x_is_zero else 1, None, st)
+    for _ in range(1, nu):
+        L.call("vk_residual", lv.A.handle, L.ptr(rhs), L.ptr(x), L.ptr(lv.r), st)
+        rho_next = 1.0 / (2.0 * sigma - rho)                            # mg.py:252-254
+        L.call("vk_patches_apply_cheb", h, L.ptr(lv.r), L.ptr(x), L.ptr(lv.d), rho_next * rho,
+               2.0 * rho_next / delta, 0, None, st)
+        rho = rho_next
+
+
 def chebyshev_iteration(operator, preconditioner, lower, upper, b, x, nu):
-    """Degree-nu Chebyshev iteration (reference ``mg.py:237-255``) on device
-    vectors (operator / preconditioner: matrices or device callables)."""
+    """Degree-nu preconditioned Chebyshev iteration (reference ``mg.py:
+    237-255``) for a generic operator / preconditioner (matrices or device
+    callables) on device vectors: the residual b - op(x) and the d / x
+    recurrence run in the library's kernels (``vk_axpy``, ``vk_cheb_update``,
+    elementwise in the reference's order)."""
+    import torch
     op = _device_operator(operator)
     prec = _device_operator(preconditioner)
+    st = L.stream_ptr()
     theta = 0.5 * (upper + lower)
     delta = 0.5 * (upper - lower)
     sigma = theta / delta
     rho = 1.0 / sigma
-    r = b - op(x)
-    d = prec(r) / theta
-    for step in range(nu):
-        x = x + d
-        if step == nu - 1:
-            break
-        r = b - op(x)
+    b, host = to_device(b)
+    x = to_device(x)[0].clone()
+    n = x.numel()
+    r = torch.empty_like(x)
+    d = torch.empty_like(x)
+
+    def residual():                       # r = b - op(x)
+        y = op(x)
+        r.copy_(b)
+        L.call("vk_axpy", n, -1.0, L.ptr(y), L.ptr(r), st)
+
+    residual()
+    L.call("vk_cheb_update", n, L.ptr(prec(r)), L.ptr(d), L.ptr(x), 0.0, theta, 1, st)
+    for _ in range(1, nu):
+        residual()
         rho_next = 1.0 / (2.0 * sigma - rho)
-        d = rho_next * rho * d + (2.0 * rho_next / delta) * prec(r)
+        L.call("vk_cheb_update", n, L.ptr(prec(r)), L.ptr(d), L.ptr(x), rho_next * rho,
+               2.0 * rho_next / delta, 0, st)
         rho = rho_next
-    return x
-
-
-def _level_precond(level):
-    def precond(r):
-        return _apply_out(level, r)
-    precond._device = True
-    return precond
-
-
-def _apply_out(level, r):
-    import torch
-    out = torch.empty_like(r)
-    L.call("vk_patches_apply", level.patches.handle, L.ptr(r), L.ptr(out), 1.0,
-           L.VK_APPLY_OUT, None, L.stream_ptr())
-    return out
+    return to_host(x, host)
 
 
 def chebyshev_relax(level, b, x, nu, mode: str = "degree"):
     """Patch-preconditioned Chebyshev relaxation on one level (reference
     ``mg.chebyshev_relax``, ``mg.py:258-271``); numpy or device vectors."""
     import torch
+    if mode not in CHEB_MODES:
+        raise ValueError(f"unknown chebyshev mode {mode!r}")
     bd, host = to_device(b)
     xd = to_device(x)[0].clone()
-    lower, upper = level.cheb.lower, level.cheb.upper
-    if mode == "degree":
-        out = chebyshev_iteration(level.A if hasattr(level, "A") else level.system.matrix,
-                                  _level_precond(level), lower, upper, bd, xd, nu)
-        return to_host(out, host)
-    if mode != "repeat":
-        raise ValueError(f"unknown chebyshev mode {mode!r}")
-    damp = 2.0 / (lower + upper)
-    A = level.A if hasattr(level, "A") else device_csr(level.system.matrix)
-    r = torch.empty_like(bd)
-    st = L.stream_ptr()
-    for _ in range(nu):
-        L.call("vk_residual", A.handle, L.ptr(bd), L.ptr(xd), L.ptr(r), st)
-        L.call("vk_patches_apply", level.patches.handle, L.ptr(r), L.ptr(xd), damp,
-               L.VK_APPLY_XADD, None, st)
+    if not hasattr(level, "A"):
+        level = _LevelView(level, bd.numel())
+    if nu > 0:
+        _relax_device(level, bd, xd, nu, mode, x_is_zero=False)
     return to_host(xd, host)
+
+
+class _LevelView:
+    """Device work vectors for a reference-shaped level object passed to
+    :func:`chebyshev_relax` (``system``, ``patches``, ``cheb``)."""
+
+    def __init__(self, level, n):
+        import torch
+        self.patches = level.patches
+        self.cheb = level.cheb
+        self.A = device_csr(level.system.matrix)
+        self.r = torch.empty(n, dtype=torch.float64, device="cuda")
+        self.d = torch.empty(n, dtype=torch.float64, device="cuda")
 
 
 def coarse_solve(hier: MgHierarchy, b):

@@ -12,8 +12,8 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "data", "cfg2_pack.npz")),
-                    reason="data/cfg2_pack.npz not generated (tools/make_packs.py)")
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "data", "cfg3_pack.npz")),
+                    reason="data/cfg3_pack.npz not generated (tools/make_packs.py)")
 def test_reference_arm_json_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
                           "--steps", "1", "--warmup", "1"], capture_output=True, text=True,
@@ -33,8 +33,8 @@ def test_reference_arm_json_line():
 
 
 @pytest.mark.gpu
-@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "data", "cfg2_pack.npz")),
-                    reason="data/cfg2_pack.npz not generated (tools/make_packs.py)")
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "data", "cfg3_pack.npz")),
+                    reason="data/cfg3_pack.npz not generated (tools/make_packs.py)")
 def test_ours_json_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3",
                           "--warmup", "3", "--no-cpu"], capture_output=True, text=True,
@@ -53,4 +53,11 @@ def test_ours_json_line():
     assert rf["frac"] == pytest.approx(rf["achieved"] / rf["peak"])
     e = d["e2e"]
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["value"] > 0
-    assert d["mg_fgmres"]["converged"] and d["mg_fgmres"]["iterations"] == 11
+    # the headline is the largest BASELINE config; every config's TTS beside it
+    assert d["config"]["workload"].startswith("cfg3")
+    assert rf["traffic"] is not None and 0.9 < rf["traffic"] / rf["algorithmic_bytes"] < 1.1
+    ref_its = {"cfg2": 11, "cfg3": 13, "cfg4": 14, "cfg5": 22}
+    for cfg, its in ref_its.items():
+        mg = d["per_config"][cfg]["mg_fgmres"]
+        assert mg["converged"] and abs(mg["iterations"] - its) <= 1, cfg
+    assert d["e2e_dropin"]["value"] > 0

@@ -7,8 +7,9 @@ and its MG-FGMRES(30) history with those bounds, for both Chebyshev modes.
 
 Gates: lam relative 1e-10 (10 Arnoldi steps on operators that differ from
 the reference by ~1e-16 per application); history as test_gpu_parity:
-iterations +-1 and max(1e-10, SELFVAR_FACTOR * the reference's own
-1-vs-8-BLAS-thread history variation recorded in the golden).
+iterations +-1 and max(1e-10, the reference's own floor recorded in the
+golden: the largest history change the reference shows when only its coarse
+solve is replaced by another valid factorization).
 """
 
 import json
@@ -22,7 +23,6 @@ from conftest import GOLDEN, load_case
 RUNS = sorted(f[:-len("_spectra.json")] for f in os.listdir(GOLDEN) if f.endswith("_spectra.json"))
 REL_LAM = 1e-10
 REL_HIST = 1e-10
-SELFVAR_FACTOR = 4.0
 
 
 def _golden(run):
@@ -56,11 +56,11 @@ def test_device_spectra_and_fgmres(run, capsys):
     m = min(len(hist), len(ref))
     rel = float(np.max(np.abs(hist[:m] - ref[:m]) / ref[:m]))
     floor = g["selfvar_history_max_rel"]
-    tol = max(REL_HIST, SELFVAR_FACTOR * floor)
+    tol = max(REL_HIST, floor)
     with capsys.disabled():
         print(f"\n[{run}] lam rel {rel_lam:.2e}; iterations {its} (ref {g['iterations']}); "
               f"history rel {rel:.2e} (strict 1e-10: {'pass' if rel <= REL_HIST else 'FAIL'}; "
-              f"reference self-variation {floor:.2e}; tolerance {tol:.2e})")
+              f"reference floor {floor:.2e}; tolerance {tol:.2e})")
     assert rel_lam <= REL_LAM
     assert conv and abs(its - g["iterations"]) <= 1
     assert rel <= tol
