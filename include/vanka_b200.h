@@ -71,6 +71,11 @@ VK_API int vk_csr_create(const int32_t* indptr, const int32_t* indices, const do
 VK_API int vk_csr_transpose(vk_csr_t a, vk_csr_t* out);
 VK_API int vk_csr_info(vk_csr_t a, int32_t* nrows, int32_t* ncols, int64_t* nnz);
 VK_API int vk_csr_destroy(vk_csr_t a);
+/* copy a CSR to HOST arrays (any may be NULL): indptr[nrows+1], indices[nnz],
+ * data[nnz] (scipy layout, sorted indices) */
+VK_API int vk_csr_export(vk_csr_t a, int32_t* indptr, int32_t* indices, double* data);
+/* max |a_ij| over the stored entries (the coarse shift of mg.py:231) */
+VK_API int vk_csr_max_abs(vk_csr_t a, double* out_host);
 
 /* ---------------- SpMV (K5/K6) ---------------------------------------------
  * y = alpha*A x + beta*y   : sparsela.spmv (sparsela.py:45-47), prolong
@@ -209,6 +214,48 @@ VK_API int vk_combine(int64_t n, int32_t count, const double* z, const double* c
                double* x, void* stream);
 /* dense[rows x cols] (row-major, device) = CSR (coarse operator densify) */
 VK_API int vk_csr_to_dense(vk_csr_t a, double* dense, void* stream);
+
+/* ---------------- device assembly ------------------------
+ * replaces assembly.py:93-172, 230-285 (operator) and mg.py:127-167
+ * (prolongation).  The host passes reference-cell data only; COO entries
+ * are written at fixed positions (cell-major / facet-major / in the
+ * reference's prolongation loop order) into caller-owned DEVICE buffers
+ * keys[] (row * ncols + col) and vals[].
+ * vk_assemble_cells: per cell, the velocity block 2 nu (eps u, eps v) and
+ *   both divergence blocks -(div v, p) (nv*nv + 2*np*nv entries per cell);
+ *   rv/rg: reference velocity basis values / gradients at the nq points
+ *   ([nq][nv][2], [nq][nv][2][2]); pv [nq][np]; cell_xy [ncells][3|4][2] in
+ *   reference-map vertex order; piola: H(div) contravariant map.
+ * vk_assemble_facets: per interior edge the (2nv)^2 block of the H(div)
+ *   consistency / symmetry / penalty terms (assembly.py:243-267); rv/rg
+ *   [6][nq][nv][..] tables per (local edge slot, aligned); info [ne][6] =
+ *   c1, c2, slot1, aligned1, slot2, aligned2; geo [ne][5] = t, n1, h_e.
+ * vk_prolong_entries: per (parent, child slot) the block (sc/sf) E[cfg]
+ *   (mg.py:141-147) in loop order.
+ * vk_coo_to_csr: stable sort by (row, col); duplicates summed in generation
+ *   order (dup_first = 0) or the first kept (dup_first = 1, mg.py:149-153);
+ *   entries with |v| <= drop_abs, in row_drop rows or col_drop columns are
+ *   removed; rows flagged in diag_one become identity rows (the buffers then
+ *   need n + nrows entries).  Synchronous; *out is a new CSR handle. */
+VK_API int vk_assemble_cells(int32_t ncells, int32_t nq, int32_t nv, int32_t np, int32_t quad,
+                             int32_t piola, const double* w, const double* pts, const double* rv,
+                             const double* rg, const double* pv, const double* cell_xy,
+                             const int32_t* vdofs, const double* vscale, const int32_t* pdofs,
+                             const double* pscale, int32_t poffset, double viscosity,
+                             int64_t ncols, int64_t* keys, double* vals, void* stream);
+VK_API int vk_assemble_facets(int32_t nedges, int32_t nq, int32_t nv, const double* w,
+                              const double* rv, const double* rg, const int32_t* info,
+                              const double* geo, const double* cell_xy, const int32_t* vdofs,
+                              const double* vscale, double viscosity, double alpha,
+                              int64_t ncols, int64_t* keys, double* vals, void* stream);
+VK_API int vk_prolong_entries(int32_t nparent, int32_t nf, int32_t nc, const int32_t* children,
+                              const int32_t* cfg, const double* tables, const int32_t* cdofs,
+                              const double* cscale, const int32_t* fdofs, const double* fscale,
+                              int64_t row_off, int64_t col_off, int64_t ncols, int64_t* keys,
+                              double* vals, void* stream);
+VK_API int vk_coo_to_csr(int64_t n, int64_t* keys, double* vals, int32_t nrows, int32_t ncols,
+                         int32_t dup_first, double drop_abs, const uint8_t* row_drop,
+                         const uint8_t* col_drop, const uint8_t* diag_one, vk_csr_t* out);
 
 /* ---------------- coarse dense operator and its inverse --------------------
  * replaces the reference's coarse factorization (mg.py:228-232:

@@ -19,5 +19,7 @@ from .vanka import (EntityRef, Patch, PatchSet, SweepStream, apply_additive, bui
 from .mg import (ChebyshevParams, FixedDamping, Level, MgHierarchy, TransferPair,
                  chebyshev_iteration, chebyshev_relax, coarse_solve, hierarchy_from_pack,
                  hierarchy_from_reference, make_preconditioner, pressure_kernel, v_cycle)
+from .assembly import ProblemConfig, assemble, build_hierarchy, build_prolongation
+from .fem import build_mixed, strong_bc, structured_mesh
 
 __version__ = "0.1.0"

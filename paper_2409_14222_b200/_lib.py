@@ -36,6 +36,8 @@ SIGNATURES = {
     "vk_csr_transpose": (C.c_int, [_p, C.POINTER(_p)]),
     "vk_csr_info": (C.c_int, [_p, _P_i32, _P_i32, C.POINTER(_i64)]),
     "vk_csr_destroy": (C.c_int, [_p]),
+    "vk_csr_max_abs": (C.c_int, [_p, _p]),
+    "vk_csr_export": (C.c_int, [_p, _p, _p, _p]),
     "vk_spmv": (C.c_int, [_p, _p, _p, _f64, _f64, _p]),
     "vk_residual": (C.c_int, [_p, _p, _p, _p, _p]),
     "vk_residual_restrict": (C.c_int, [_p, _p, _p, _p, _p, _p, _p]),
@@ -67,6 +69,14 @@ SIGNATURES = {
     "vk_gemv": (C.c_int, [_i32, _i32, _p, _p, _p, _p]),
     "vk_combine": (C.c_int, [_i64, _i32, _p, _p, _p, _p]),
     "vk_csr_to_dense": (C.c_int, [_p, _p, _p]),
+    "vk_assemble_cells": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p,
+                                    _p, _p, _p, _p, _i32, _f64, _i64, _p, _p, _p]),
+    "vk_assemble_facets": (C.c_int, [_i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _f64,
+                                     _f64, _i64, _p, _p, _p]),
+    "vk_prolong_entries": (C.c_int, [_i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _i64,
+                                     _i64, _p, _p, _p]),
+    "vk_coo_to_csr": (C.c_int, [_i64, _p, _p, _i32, _i32, _i32, _f64, _p, _p, _p,
+                                C.POINTER(_p)]),
     "vk_coarse_operator": (C.c_int, [_p, _p, _f64, _p, _p]),
     "vk_dense_inverse_workspace": (C.c_int64, [_i32]),
     "vk_dense_inverse": (C.c_int, [_i32, _p, _p, _p, _P_i32, _P_i32, _p]),

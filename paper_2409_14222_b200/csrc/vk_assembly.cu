@@ -1,0 +1,506 @@
+// Device assembly of the global saddle-point CSR and of the natural-embedding
+// prolongation.
+//
+// Replaces the reference's setup path:
+//   assembly.py:136-172  cell terms 2 nu (eps u, eps v) and -(div v, p)
+//   assembly.py:230-270  H(div) interior-facet consistency / symmetrisation /
+//                        alpha / h_e tangential-jump penalty
+//   assembly.py:93-129   COO accumulation and summation into CSR
+//   assembly.py:273-285  symmetric strong-BC elimination (identity rows)
+//   mg.py:127-167        build_prolongation (first-occurrence dedup, |v| >
+//                        1e-12) and _mask_transfer
+//
+// The host supplies only O(1) reference-cell data (quadrature, reference basis
+// values / gradients at the quadrature points, the prolongation blocks of the
+// few parent/child configurations of a structured refinement) and the integer
+// DoF maps; every per-cell / per-facet matrix, the push-forward by each cell's
+// Jacobian, the COO scatter, sorting, duplicate summation, boundary
+// elimination and CSR construction run here.  Deterministic: entries are
+// generated at fixed positions (cell-major, then facets), sorted by a stable
+// radix sort on (row, col), and duplicates are summed sequentially in that
+// order — the reference's order of accumulation per entry (cell by cell), so
+// values agree with it to rounding (its own COO flushes and index sorts fix
+// a different association on a few entries).
+#include <algorithm>
+#include <cub/cub.cuh>
+
+#include "vk_common.cuh"
+
+namespace {
+
+constexpr int kCellThreads = 256;
+
+// per-quadrature-point Jacobian of the affine (tri) / bilinear (quad) map
+__device__ __forceinline__ void jacobian(int quad, const double* __restrict__ xy, double x,
+                                         double y, double J[2][2], double& det, double inv[2][2]) {
+  const double x0 = xy[0], y0 = xy[1];
+  J[0][0] = xy[2] - x0;
+  J[1][0] = xy[3] - y0;
+  J[0][1] = xy[4] - x0;
+  J[1][1] = xy[5] - y0;
+  if (quad) {
+    const double tx = x0 - xy[2] - xy[4] + xy[6], ty = y0 - xy[3] - xy[5] + xy[7];
+    J[0][0] += y * tx;
+    J[1][0] += y * ty;
+    J[0][1] += x * tx;
+    J[1][1] += x * ty;
+  }
+  det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  inv[0][0] = J[1][1] / det;
+  inv[0][1] = -J[0][1] / det;
+  inv[1][0] = -J[1][0] / det;
+  inv[1][1] = J[0][0] / det;
+}
+
+// physical gradient (c, a) and value (c) of reference basis function data
+// rv[c], rg[c][d] under the identity (gradients by J^-T) or Piola map
+__device__ __forceinline__ void push(int piola, const double J[2][2], double det,
+                                     const double inv[2][2], const double rv[2],
+                                     const double rg[2][2], double pv[2], double pg[2][2]) {
+  if (!piola) {
+    pv[0] = rv[0];
+    pv[1] = rv[1];
+    for (int c = 0; c < 2; ++c)
+      for (int a = 0; a < 2; ++a) pg[c][a] = rg[c][0] * inv[0][a] + rg[c][1] * inv[1][a];
+    return;
+  }
+  for (int c = 0; c < 2; ++c) pv[c] = (J[c][0] * rv[0] + J[c][1] * rv[1]) / det;
+  double jg[2][2];
+  for (int c = 0; c < 2; ++c)
+    for (int b = 0; b < 2; ++b) jg[c][b] = J[c][0] * rg[0][b] + J[c][1] * rg[1][b];
+  for (int c = 0; c < 2; ++c)
+    for (int a = 0; a < 2; ++a) pg[c][a] = (jg[c][0] * inv[0][a] + jg[c][1] * inv[1][a]) / det;
+}
+
+struct CellArgs {
+  int ncells, nq, nv, np, quad, piola, nvert, poffset;
+  const double *w, *pts, *rv, *rg, *pv;   // reference data: w[nq], pts[nq][2],
+                                          // rv[nq][nv][2], rg[nq][nv][2][2], pv[nq][np]
+  const double* cell_xy;                  // [ncells][nvert][2]
+  const int *vdofs, *pdofs;
+  const double *vscale, *pscale;
+  double two_nu;
+  int64_t ncols;
+  unsigned long long* keys;
+  double* vals;
+};
+
+// One CTA per cell (grid-stride).  Shared memory: the reference tables once,
+// then per cell the strain components E[q][i][3] (eps00, eps11, eps01), the
+// divergence and w_q det_q.
+__global__ void __launch_bounds__(kCellThreads) cell_terms_kernel(CellArgs a) {
+  extern __shared__ double sm[];
+  const int nq = a.nq, nv = a.nv, np = a.np;
+  double* s_rv = sm;                                  // nq*nv*2
+  double* s_rg = s_rv + nq * nv * 2;                  // nq*nv*4
+  double* s_pv = s_rg + nq * nv * 4;                  // nq*np
+  double* s_e = s_pv + nq * np;                       // nq*nv*3
+  double* s_div = s_e + nq * nv * 3;                  // nq*nv
+  double* s_wd = s_div + nq * nv;                     // nq
+  for (int t = threadIdx.x; t < nq * nv * 2; t += blockDim.x) s_rv[t] = a.rv[t];
+  for (int t = threadIdx.x; t < nq * nv * 4; t += blockDim.x) s_rg[t] = a.rg[t];
+  for (int t = threadIdx.x; t < nq * np; t += blockDim.x) s_pv[t] = a.pv[t];
+  const int64_t per_cell = int64_t(nv) * nv + 2 * int64_t(np) * nv;
+  for (int c = blockIdx.x; c < a.ncells; c += gridDim.x) {
+    __syncthreads();
+    const double* xy = a.cell_xy + int64_t(c) * a.nvert * 2;
+    for (int t = threadIdx.x; t < nq * nv; t += blockDim.x) {
+      const int q = t / nv, i = t % nv;
+      double J[2][2], det, inv[2][2];
+      jacobian(a.quad, xy, a.pts[2 * q], a.pts[2 * q + 1], J, det, inv);
+      const double* rv = s_rv + (q * nv + i) * 2;
+      const double* rg = s_rg + (q * nv + i) * 4;
+      double rvv[2] = {rv[0], rv[1]}, rgg[2][2] = {{rg[0], rg[1]}, {rg[2], rg[3]}};
+      double pvv[2], pg[2][2];
+      push(a.piola, J, det, inv, rvv, rgg, pvv, pg);
+      s_e[t * 3 + 0] = pg[0][0];
+      s_e[t * 3 + 1] = pg[1][1];
+      s_e[t * 3 + 2] = 0.5 * (pg[0][1] + pg[1][0]);
+      s_div[t] = pg[0][0] + pg[1][1];
+      if (i == 0) s_wd[q] = a.w[q] * det;
+    }
+    __syncthreads();
+    const int* gv = a.vdofs + int64_t(c) * nv;
+    const double* sv = a.vscale + int64_t(c) * nv;
+    const int* gq = a.pdofs + int64_t(c) * np;
+    const double* sq = a.pscale + int64_t(c) * np;
+    unsigned long long* keys = a.keys + c * per_cell;
+    double* vals = a.vals + c * per_cell;
+    // velocity block: 2 nu sum_q wdet eps_i : eps_j
+    for (int t = threadIdx.x; t < nv * nv; t += blockDim.x) {
+      const int i = t / nv, j = t % nv;
+      double acc = 0.0;
+      for (int q = 0; q < nq; ++q) {
+        const double* ei = s_e + (q * nv + i) * 3;
+        const double* ej = s_e + (q * nv + j) * 3;
+        const double e = ei[0] * ej[0] + ei[1] * ej[1] + 2.0 * (ei[2] * ej[2]);
+        acc = fma(s_wd[q], e, acc);
+      }
+      const double loc = a.two_nu * acc;
+      keys[t] = (unsigned long long)gv[i] * a.ncols + gv[j];
+      vals[t] = (sv[i] * sv[j]) * loc;
+    }
+    // divergence blocks: B[p][i] = -sum_q wdet q_p div_i, and its transpose
+    for (int t = threadIdx.x; t < np * nv; t += blockDim.x) {
+      const int p = t / nv, i = t % nv;
+      double acc = 0.0;
+      for (int q = 0; q < nq; ++q) acc = fma(s_wd[q] * s_pv[q * np + p], s_div[q * nv + i], acc);
+      const double b = -acc;
+      const int64_t row_p = int64_t(gq[p]) + a.poffset;
+      keys[nv * nv + t] = (unsigned long long)row_p * a.ncols + gv[i];
+      vals[nv * nv + t] = (sq[p] * sv[i]) * b;
+      keys[nv * nv + np * nv + t] = (unsigned long long)gv[i] * a.ncols + row_p;
+      vals[nv * nv + np * nv + t] = (sv[i] * sq[p]) * b;
+    }
+  }
+}
+
+struct FacetArgs {
+  int nedges, nq, nv;
+  const double* w;           // [nq] interval weights (times h_e inside)
+  const double *rv, *rg;     // [6][nq][nv][2], [6][nq][nv][2][2]: (slot, aligned) tables
+  const int* info;           // [nedges][6]: c1, c2, slot1, aligned1, slot2, aligned2
+  const double* geo;         // [nedges][5]: tx, ty, n1x, n1y, h_e
+  const double* cell_xy;     // [ncells][3][2]
+  const int* vdofs;
+  const double* vscale;
+  double nu, alpha;
+  int64_t ncols;
+  unsigned long long* keys;
+  double* vals;
+};
+
+// One CTA per interior edge: both sides' Piola-mapped traces, then the
+// 2nv x 2nv block of reference assembly.py:243-267.
+__global__ void __launch_bounds__(kCellThreads) facet_terms_kernel(FacetArgs a) {
+  extern __shared__ double sm[];
+  const int nq = a.nq, nv = a.nv;
+  double* s_vt = sm;                       // [2][nq][nv]      v . t
+  double* s_et = s_vt + 2 * nq * nv;       // [2 side][2 r][nq][nv]  eps : T_r
+  const int64_t per_edge = int64_t(2 * nv) * (2 * nv);
+  for (int e = blockIdx.x; e < a.nedges; e += gridDim.x) {
+    __syncthreads();
+    const int* inf = a.info + int64_t(e) * 6;
+    const double* g = a.geo + int64_t(e) * 5;
+    const double t0 = g[0], t1 = g[1], n0 = g[2], n1 = g[3], h = g[4];
+    // T_r = sym(t (x) n_r), n_0 = n1, n_1 = -n1
+    double T[2][2][2];
+    for (int r = 0; r < 2; ++r) {
+      const double sgn = r == 0 ? 1.0 : -1.0;
+      const double nx = sgn * n0, ny = sgn * n1;
+      T[r][0][0] = 0.5 * (t0 * nx + nx * t0);
+      T[r][0][1] = 0.5 * (t0 * ny + nx * t1);
+      T[r][1][0] = 0.5 * (t1 * nx + ny * t0);
+      T[r][1][1] = 0.5 * (t1 * ny + ny * t1);
+    }
+    for (int t = threadIdx.x; t < 2 * nq * nv; t += blockDim.x) {
+      const int s = t / (nq * nv), q = (t / nv) % nq, i = t % nv;
+      const int cell = inf[s], slot = inf[2 + 2 * s], al = inf[3 + 2 * s];
+      const int tab = slot * 2 + al;
+      const double* xy = a.cell_xy + int64_t(cell) * 6;
+      double J[2][2], det, inv[2][2];
+      jacobian(0, xy, 0.0, 0.0, J, det, inv);
+      const double* rv = a.rv + ((int64_t(tab) * nq + q) * nv + i) * 2;
+      const double* rg = a.rg + ((int64_t(tab) * nq + q) * nv + i) * 4;
+      double rvv[2] = {rv[0], rv[1]}, rgg[2][2] = {{rg[0], rg[1]}, {rg[2], rg[3]}};
+      double pv[2], pg[2][2];
+      push(1, J, det, inv, rvv, rgg, pv, pg);
+      s_vt[t] = pv[0] * t0 + pv[1] * t1;
+      double eps[2][2];
+      for (int c = 0; c < 2; ++c)
+        for (int b = 0; b < 2; ++b) eps[c][b] = 0.5 * (pg[c][b] + pg[b][c]);
+      for (int r = 0; r < 2; ++r) {
+        double acc = 0.0;
+        for (int c = 0; c < 2; ++c)
+          for (int b = 0; b < 2; ++b) acc += eps[c][b] * T[r][c][b];
+        s_et[((s * 2 + r) * nq + q) * nv + i] = acc;
+      }
+    }
+    __syncthreads();
+    double tt[2][2];
+    for (int s = 0; s < 2; ++s)
+      for (int r = 0; r < 2; ++r) {
+        double acc = 0.0;
+        for (int c = 0; c < 2; ++c)
+          for (int b = 0; b < 2; ++b) acc += T[s][c][b] * T[r][c][b];
+        tt[s][r] = acc;
+      }
+    const double pen = (2.0 * a.nu * a.alpha / h);
+    unsigned long long* keys = a.keys + e * per_edge;
+    double* vals = a.vals + e * per_edge;
+    const int n2 = 2 * nv;
+    for (int t = threadIdx.x; t < n2 * n2; t += blockDim.x) {
+      const int I = t / n2, Jc = t % n2;
+      const int b = I / nv, i = I % nv, aa = Jc / nv, j = Jc % nv;
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      for (int q = 0; q < nq; ++q) {
+        const double wq = a.w[q] * h;
+        const double vb = s_vt[(b * nq + q) * nv + i], va = s_vt[(aa * nq + q) * nv + j];
+        s1 = fma(wq * vb, s_et[((aa * 2 + b) * nq + q) * nv + j], s1);
+        s2 = fma(wq * s_et[((b * 2 + aa) * nq + q) * nv + i], va, s2);
+        s3 = fma(wq * vb, va, s3);
+      }
+      const double loc = (-a.nu * s1 + -a.nu * s2) + pen * tt[aa][b] * s3;
+      const int ci = inf[b], cj = inf[aa];
+      const int gi = a.vdofs[int64_t(ci) * nv + i], gj = a.vdofs[int64_t(cj) * nv + j];
+      const double si = a.vscale[int64_t(ci) * nv + i], sj = a.vscale[int64_t(cj) * nv + j];
+      keys[t] = (unsigned long long)gi * a.ncols + gj;
+      vals[t] = (si * sj) * loc;
+    }
+  }
+}
+
+// prolongation COO, in the reference's loop order (parent, child in
+// parent_cells order, fine local i, coarse local j): value = (sc_j / sf_i) E
+__global__ void prolong_entries_kernel(int nparent, int nf, int nc, const int* __restrict__ children,
+                                       const int* __restrict__ cfg, const double* __restrict__ tables,
+                                       const int* __restrict__ cdofs, const double* __restrict__ cscale,
+                                       const int* __restrict__ fdofs, const double* __restrict__ fscale,
+                                       int64_t row_off, int64_t col_off, int64_t ncols,
+                                       unsigned long long* __restrict__ keys, double* __restrict__ vals) {
+  const int64_t per = int64_t(nf) * nc;
+  const int64_t total = int64_t(nparent) * 4 * per;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t pc = e / per;                  // parent * 4 + child slot
+    const int rem = static_cast<int>(e - pc * per);
+    const int i = rem / nc, j = rem % nc;
+    const int parent = static_cast<int>(pc / 4);
+    const int child = children[pc];
+    const double ent = tables[(int64_t(cfg[pc]) * nf + i) * nc + j];
+    const double sc = cscale[int64_t(parent) * nc + j], sf = fscale[int64_t(child) * nf + i];
+    keys[e] = (unsigned long long)(fdofs[int64_t(child) * nf + i] + row_off) * ncols +
+              (cdofs[int64_t(parent) * nc + j] + col_off);
+    vals[e] = (sc / sf) * ent;
+  }
+}
+
+// ---- COO -> CSR --------------------------------------------------------------
+
+__global__ void diag_entries_kernel(int nrows, const uint8_t* __restrict__ diag_one, int64_t ncols,
+                                    int64_t base, unsigned long long* __restrict__ keys,
+                                    double* __restrict__ vals, int64_t* __restrict__ count) {
+  // appended (r, r) placeholders for rows that become identity rows
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    if (!diag_one[r]) continue;
+    const int64_t slot = base + atomicAdd(reinterpret_cast<unsigned long long*>(count), 1ull);
+    keys[slot] = (unsigned long long)r * ncols + r;
+    vals[slot] = 0.0;
+  }
+}
+
+// per unique key (segment head): the reduced value and whether it survives
+__global__ void reduce_segments_kernel(int64_t n, const unsigned long long* __restrict__ keys,
+                                       const double* __restrict__ vals, int64_t ncols, int dup_first,
+                                       double drop_abs, const uint8_t* __restrict__ row_drop,
+                                       const uint8_t* __restrict__ col_drop,
+                                       const uint8_t* __restrict__ diag_one,
+                                       double* __restrict__ out_val, int* __restrict__ keep) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long key = keys[k];
+    if (k > 0 && keys[k - 1] == key) {
+      keep[k] = 0;
+      continue;
+    }
+    double v = vals[k];
+    if (!dup_first)
+      for (int64_t m = k + 1; m < n && keys[m] == key; ++m) v = __dadd_rn(v, vals[m]);
+    const int64_t r = static_cast<int64_t>(key / ncols), c = static_cast<int64_t>(key % ncols);
+    int kp;
+    if (diag_one && diag_one[r]) {
+      kp = (r == c);
+      v = 1.0;
+    } else {
+      kp = !(fabs(v) <= drop_abs) && !(row_drop && row_drop[r]) && !(col_drop && col_drop[c]);
+    }
+    keep[k] = kp;
+    out_val[k] = v;
+  }
+}
+
+__global__ void scatter_csr_kernel(int64_t n, const unsigned long long* __restrict__ keys,
+                                   const double* __restrict__ rv, const int* __restrict__ keep,
+                                   const int* __restrict__ pos, int64_t ncols,
+                                   int* __restrict__ rows_out, int* __restrict__ cols,
+                                   double* __restrict__ data, int* __restrict__ rowcount) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    if (!keep[k]) continue;
+    const int p = pos[k];
+    const int r = static_cast<int>(keys[k] / ncols);
+    cols[p] = static_cast<int>(keys[k] % ncols);
+    data[p] = rv[k];
+    rows_out[p] = r;
+    atomicAdd(rowcount + r + 1, 1);
+  }
+}
+
+template <typename T>
+T* dalloc(size_t n, cudaError_t& e) {
+  T* p = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1));
+  return p;
+}
+
+int bits_for(unsigned long long v) {
+  int b = 1;
+  while (b < 64 && (1ull << b) <= v) ++b;
+  return b;
+}
+
+}  // namespace
+
+extern "C" int vk_assemble_cells(int32_t ncells, int32_t nq, int32_t nv, int32_t np, int32_t quad,
+                                 int32_t piola, const double* w, const double* pts,
+                                 const double* rv, const double* rg, const double* pv,
+                                 const double* cell_xy, const int32_t* vdofs,
+                                 const double* vscale, const int32_t* pdofs,
+                                 const double* pscale, int32_t poffset, double viscosity,
+                                 int64_t ncols, int64_t* keys, double* vals, void* stream) {
+  VK_REQUIRE(ncells >= 0 && nq > 0 && nv > 0 && np >= 0 && w && pts && rv && rg && cell_xy &&
+                 vdofs && vscale && keys && vals && (np == 0 || (pv && pdofs && pscale)),
+             "vk_assemble_cells: bad argument");
+  if (ncells == 0) return VK_OK;
+  CellArgs a{ncells, nq, nv, np, quad, piola, quad ? 4 : 3, poffset, w, pts, rv, rg, pv, cell_xy,
+             vdofs, pdofs, vscale, pscale, 2.0 * viscosity, ncols,
+             reinterpret_cast<unsigned long long*>(keys), vals};
+  const size_t smem = sizeof(double) * (size_t(nq) * nv * (2 + 4 + 3 + 1) + size_t(nq) * np + nq);
+  VK_REQUIRE(smem <= 200 * 1024, "vk_assemble_cells: tables too large (%zu bytes)", smem);
+  VK_CHECK_CUDA(vk_smem_optin((const void*)cell_terms_kernel, int(smem)));
+  const int grid = std::min(ncells, vk_resident_blocks((const void*)cell_terms_kernel,
+                                                       kCellThreads, smem));
+  cell_terms_kernel<<<grid, kCellThreads, smem, vk_stream(stream)>>>(a);
+  VK_CHECK_LAUNCH();
+  return VK_OK;
+}
+
+extern "C" int vk_assemble_facets(int32_t nedges, int32_t nq, int32_t nv, const double* w,
+                                  const double* rv, const double* rg, const int32_t* info,
+                                  const double* geo, const double* cell_xy, const int32_t* vdofs,
+                                  const double* vscale, double viscosity, double alpha,
+                                  int64_t ncols, int64_t* keys, double* vals, void* stream) {
+  VK_REQUIRE(nedges >= 0 && nq > 0 && nv > 0 && w && rv && rg && info && geo && cell_xy &&
+                 vdofs && vscale && keys && vals,
+             "vk_assemble_facets: bad argument");
+  if (nedges == 0) return VK_OK;
+  FacetArgs a{nedges, nq, nv, w, rv, rg, info, geo, cell_xy, vdofs, vscale, viscosity, alpha,
+              ncols, reinterpret_cast<unsigned long long*>(keys), vals};
+  const size_t smem = sizeof(double) * size_t(nq) * nv * 6;
+  VK_REQUIRE(smem <= 200 * 1024, "vk_assemble_facets: tables too large");
+  VK_CHECK_CUDA(vk_smem_optin((const void*)facet_terms_kernel, int(smem)));
+  const int grid = std::min(nedges, vk_resident_blocks((const void*)facet_terms_kernel,
+                                                       kCellThreads, smem));
+  facet_terms_kernel<<<grid, kCellThreads, smem, vk_stream(stream)>>>(a);
+  VK_CHECK_LAUNCH();
+  return VK_OK;
+}
+
+extern "C" int vk_prolong_entries(int32_t nparent, int32_t nf, int32_t nc, const int32_t* children,
+                                  const int32_t* cfg, const double* tables, const int32_t* cdofs,
+                                  const double* cscale, const int32_t* fdofs, const double* fscale,
+                                  int64_t row_off, int64_t col_off, int64_t ncols, int64_t* keys,
+                                  double* vals, void* stream) {
+  VK_REQUIRE(nparent >= 0 && nf > 0 && nc > 0 && children && cfg && tables && cdofs && cscale &&
+                 fdofs && fscale && keys && vals,
+             "vk_prolong_entries: bad argument");
+  const int64_t total = int64_t(nparent) * 4 * nf * nc;
+  if (total == 0) return VK_OK;
+  prolong_entries_kernel<<<vk_grid(total, 256, 148 * 16), 256, 0, vk_stream(stream)>>>(
+      nparent, nf, nc, children, cfg, tables, cdofs, cscale, fdofs, fscale, row_off, col_off,
+      ncols, reinterpret_cast<unsigned long long*>(keys), vals);
+  VK_CHECK_LAUNCH();
+  return VK_OK;
+}
+
+extern "C" int vk_coo_to_csr(int64_t n, int64_t* keys, double* vals, int32_t nrows, int32_t ncols,
+                             int32_t dup_first, double drop_abs, const uint8_t* row_drop,
+                             const uint8_t* col_drop, const uint8_t* diag_one, vk_csr_t* out) {
+  VK_REQUIRE(out && n >= 0 && nrows >= 0 && ncols >= 0 && (n == 0 || (keys && vals)),
+             "vk_coo_to_csr: bad argument");
+  cudaStream_t st = 0;
+  cudaError_t e = cudaSuccess;
+  const char* step = "alloc";
+  unsigned long long* k0 = reinterpret_cast<unsigned long long*>(keys);
+  // identity rows: placeholders appended behind the n entries (the caller's
+  // buffers hold n + nrows entries when diag_one is given)
+  int64_t* d_count = dalloc<int64_t>(1, e);
+  int64_t ndiag = 0;
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_count, 0, sizeof(int64_t), st);
+  if (diag_one && nrows > 0 && e == cudaSuccess) {
+    diag_entries_kernel<<<vk_grid(nrows, 256), 256, 0, st>>>(nrows, diag_one, ncols, n, k0, vals,
+                                                            d_count);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(&ndiag, d_count, sizeof(int64_t), cudaMemcpyDeviceToHost);
+  }
+  const int64_t m = n + ndiag;
+  unsigned long long* k1 = dalloc<unsigned long long>(m, e);
+  double* v1 = dalloc<double>(m, e);
+  double* rv = dalloc<double>(m, e);
+  int* keep = dalloc<int>(m + 1, e);
+  int* pos = dalloc<int>(m + 1, e);
+  const int end_bit = bits_for((unsigned long long)std::max(nrows, 1) * std::max(ncols, 1));
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0, tb2 = 0;
+  if (e == cudaSuccess) step = "sort size";
+  if (e == cudaSuccess)
+    e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, vals, v1, m, 0, end_bit, st);
+  if (e == cudaSuccess) step = "scan size";
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(nullptr, tb2, keep, pos, m + 1, st);
+  tmp_bytes = std::max(tmp_bytes, tb2);
+  if (e == cudaSuccess) step = "tmp alloc";
+  if (e == cudaSuccess) e = cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 1));
+  if (e == cudaSuccess) step = "sort";
+  // stable sort by (row, col): duplicates stay in generation order
+  if (e == cudaSuccess && m > 0)
+    e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, vals, v1, m, 0, end_bit, st);
+  if (e == cudaSuccess) step = "reduce";
+  if (e == cudaSuccess && m > 0) {
+    reduce_segments_kernel<<<vk_grid(m, 256, 148 * 16), 256, 0, st>>>(
+        m, k1, v1, ncols, dup_first, drop_abs, row_drop, col_drop, diag_one, rv, keep);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) step = "scan";
+  if (e == cudaSuccess) e = cudaMemsetAsync(keep + m, 0, sizeof(int), st);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, keep, pos, m + 1, st);
+  int nnz = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&nnz, pos + m, sizeof(int), cudaMemcpyDeviceToHost);
+  int* rows = dalloc<int>(nnz, e);
+  int* cols = dalloc<int>(nnz, e);
+  double* data = dalloc<double>(nnz, e);
+  int* indptr = dalloc<int>(size_t(nrows) + 1, e);
+  if (e == cudaSuccess) e = cudaMemsetAsync(indptr, 0, sizeof(int) * (size_t(nrows) + 1), st);
+  if (e == cudaSuccess) step = "scatter";
+  if (e == cudaSuccess && m > 0) {
+    scatter_csr_kernel<<<vk_grid(m, 256, 148 * 16), 256, 0, st>>>(m, k1, rv, keep, pos, ncols,
+                                                                 rows, cols, data, indptr);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) step = "indptr";
+  if (e == cudaSuccess)
+    e = cub::DeviceScan::InclusiveSum(nullptr, tb2, indptr, indptr, nrows + 1, st);
+  void* tmp2 = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&tmp2, std::max<size_t>(tb2, 1));
+  if (e == cudaSuccess) e = cub::DeviceScan::InclusiveSum(tmp2, tb2, indptr, indptr, nrows + 1, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  int rc = VK_OK;
+  if (e != cudaSuccess) {
+    vk::set_error("vk_coo_to_csr (%s): %s", step, cudaGetErrorString(e));
+    rc = VK_ERR_CUDA;
+  } else {
+    rc = vk_csr_create(indptr, cols, data, nrows, ncols, nnz, out);
+  }
+  cudaFree(d_count);
+  cudaFree(k1);
+  cudaFree(v1);
+  cudaFree(rv);
+  cudaFree(keep);
+  cudaFree(pos);
+  cudaFree(tmp);
+  cudaFree(tmp2);
+  cudaFree(rows);
+  cudaFree(cols);
+  cudaFree(data);
+  cudaFree(indptr);
+  return rc;
+}

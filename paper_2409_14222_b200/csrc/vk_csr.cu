@@ -604,3 +604,26 @@ extern "C" int vk_prolong_residual(vk_csr_t p, const double* xc, double* x, vk_c
   }
   return VK_OK;
 }
+
+extern "C" int vk_csr_max_abs(vk_csr_t a, double* out_host) {
+  VK_REQUIRE(a && out_host, "vk_csr_max_abs: null argument");
+  std::vector<double> d(a->nnz);
+  if (a->nnz)
+    VK_CHECK_CUDA(cudaMemcpy(d.data(), a->data, sizeof(double) * a->nnz, cudaMemcpyDeviceToHost));
+  double m = 0.0;
+  for (double v : d) m = std::max(m, std::fabs(v));
+  *out_host = m;
+  return VK_OK;
+}
+
+extern "C" int vk_csr_export(vk_csr_t a, int32_t* indptr, int32_t* indices, double* data) {
+  VK_REQUIRE(a, "vk_csr_export: null handle");
+  if (indptr)
+    VK_CHECK_CUDA(cudaMemcpy(indptr, a->indptr, sizeof(int32_t) * (a->nrows + 1),
+                             cudaMemcpyDeviceToHost));
+  if (indices && a->nnz)
+    VK_CHECK_CUDA(cudaMemcpy(indices, a->indices, sizeof(int32_t) * a->nnz, cudaMemcpyDeviceToHost));
+  if (data && a->nnz)
+    VK_CHECK_CUDA(cudaMemcpy(data, a->data, sizeof(double) * a->nnz, cudaMemcpyDeviceToHost));
+  return VK_OK;
+}

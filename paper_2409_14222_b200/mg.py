@@ -107,6 +107,16 @@ def pressure_kernel(mixed) -> np.ndarray:
     return vec / np.linalg.norm(vec)
 
 
+def _max_abs(matrix) -> float:
+    """max |a_ij| of a host (scipy) or device CSR."""
+    import ctypes as C
+    if isinstance(matrix, DeviceCSR):
+        out = C.c_double()
+        L.call("vk_csr_max_abs", matrix.handle, C.byref(out))
+        return float(out.value)
+    return float(np.max(np.abs(matrix.data)))
+
+
 def coarse_inverse(a0, q, shift: float):
     """Explicit inverse of the coarse operator A0 + shift q q^T (reference
     ``mg.build_hierarchy``, ``mg.py:228-232``, which LU-factors it), formed
@@ -147,7 +157,7 @@ class MgHierarchy:
         self.cheb_mode = cheb_mode
         c = levels[0]
         q = torch.from_numpy(np.ascontiguousarray(coarse_kernel)).cuda()
-        shift = float(np.max(np.abs(c.system.matrix.data)))            # mg.py:231
+        shift = _max_abs(c.system.matrix)                               # mg.py:231
         self.coarse_inverse = coarse_inverse(c.A, q, shift)             # mg.py:232
         self.coarse_factor = self.coarse_inverse
         self.q = q

@@ -137,6 +137,14 @@ class DeviceCSR:
     def __matmul__(self, x):
         return self.matvec(x)
 
+    def to_scipy(self):
+        """Host scipy copy (bit-exact)."""
+        indptr = np.zeros(self.shape[0] + 1, dtype=np.int32)
+        indices = np.zeros(self.nnz, dtype=np.int32)
+        data = np.zeros(self.nnz, dtype=np.float64)
+        L.call("vk_csr_export", self._h, L.ptr(indptr), L.ptr(indices), L.ptr(data))
+        return sp.csr_matrix((data, indices, indptr), shape=self.shape)
+
     def todense_device(self):
         torch = _torch()
         d = torch.empty(self.shape, dtype=torch.float64, device="cuda")
