@@ -289,13 +289,350 @@ __global__ void extract_kernel(const int* __restrict__ ptr, const int* __restric
   }
 }
 
+// ---------------------------------------------------------------------------
+// Blocked Gauss-Jordan with FP64 tensor-core (DMMA) updates and look-ahead for
+// the large classes, 64 < s <= S (S = 80 / 96 / 104 / 112 / 128).  The block
+// lives in shared memory, padded to S with an identity tail (which stays
+// decoupled); the columns are processed in panels of 8:
+//   * panel factorisation (warp 0, registers; rows lane + 32q): the 8
+//     Gauss-Jordan steps on the panel columns of ALL rows — pivot search over
+//     the open positions with LAPACK's first-maximum tie-break (redux.sync on
+//     the |value| bits, then the lowest position), the reference guard
+//     |pivot| >= 1e-12 rowscale (sparsela.py:79-83), pivot-row broadcast by
+//     shuffles and the per-element step of the unblocked kernels (scaled
+//     pivot row, fma(-f, p_j, a), -f/pivot in the pivot column); rows never
+//     move: warp 0 keeps every row's position in registers for the patch;
+//   * panel update: every other column tile becomes
+//     C = (pivot row of the panel ? 0 : C) + Pn R, R = the panel's 8 pivot
+//     rows before the update — the in-place Gauss-Jordan elimination of 8
+//     columns in GEMM form (2 S^2 8 flops), on DMMA m8n8k4 (mma.sync .f64),
+//     8 x 8 tiles;
+//   * look-ahead: while warps 1..7 update the block with panel p, warp 0
+//     updates panel p+1's own column tile with panel p and factors panel p+1,
+//     so the latency chain of the pivot steps overlaps the tensor-core
+//     updates.  Two CTA barriers per 8 columns (vs two per column).
+// Results agree with the unblocked kernels to rounding (the elimination is
+// associated per panel); pivots and guard verdicts are those of getrf up to
+// exact near-ties.
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int S>
+__host__ __device__ constexpr size_t dmma_smem_bytes() {
+  // W, two panel buffers, two pivot-row buffers, row scales; ints: sidx,
+  // rowoff, rowk0, perm, posof, two isp flag arrays
+  return sizeof(double) * (size_t(S) * (S + 1) + 2 * size_t(S) * 8 + 2 * 8 * size_t(S + 1) + S) +
+         sizeof(int) * (7 * size_t(S) + 1);
+}
+
+// one 8x8 tile of the panel update: C = (pivot row ? 0 : C) + Pn R
+__device__ __forceinline__ void panel_update_tile(double* W, int LD, const double* Pb,
+                                                  const double* Rb, const int* isp, int ti, int tj,
+                                                  int lane) {
+  const int row = ti * 8 + (lane >> 2);
+  const int cc = tj * 8 + 2 * (lane & 3);
+  const bool zr = isp[row] != 0;
+  double c0 = zr ? 0.0 : W[row * LD + cc];
+  double c1 = zr ? 0.0 : W[row * LD + cc + 1];
+  const double a0 = Pb[row * 8 + (lane & 3)], a1 = Pb[row * 8 + 4 + (lane & 3)];
+  const double b0 = Rb[(lane & 3) * LD + tj * 8 + (lane >> 2)];
+  const double b1 = Rb[(4 + (lane & 3)) * LD + tj * 8 + (lane >> 2)];
+  dmma_8x8x4(c0, c1, a0, b0);
+  dmma_8x8x4(c0, c1, a1, b1);
+  W[row * LD + cc] = c0;
+  W[row * LD + cc + 1] = c1;
+}
+
+// warp 0: the 8 Gauss-Jordan steps of the panel at k0 (columns k0..k0+7 of
+// all S rows, in registers); the pivot row and the row at position k are
+// found by warp reductions over the positions held in registers.  Writes the
+// factored panel to W and Pb, the pivot rows to pids / isp.  Returns
+// VK_PATCH_SMALL_PIVOT on a failed guard.
+template <int S, int R>
+__device__ __forceinline__ int factor_panel(double* W, double* Pb, int (&pos)[R], int* isp,
+                                            int* pids, const double* rs, int k0, int lane) {
+  constexpr int LD = S + 1, NB = 8;
+  double pan[R][NB];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int r = lane + 32 * q;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) pan[q][c] = (r < S) ? W[r * LD + k0 + c] : 0.0;
+  }
+#pragma unroll
+  for (int kk = 0; kk < NB; ++kk) {
+    const int k = k0 + kk;
+    double best = -1.0;
+    int bpos = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const double v = fabs(pan[q][kk]);
+      if (pos[q] >= k && pos[q] < S && (v > best || (v == best && pos[q] < bpos))) {
+        best = v;
+        bpos = pos[q];
+      }
+    }
+    const unsigned long long key =
+        best >= 0.0 ? static_cast<unsigned long long>(__double_as_longlong(best)) : 0ull;
+    const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+    const int ppos = static_cast<int>(__reduce_min_sync(
+        0xffffffffu, (hi == mhi && lo == mlo) ? static_cast<unsigned>(bpos) : 0x7fffffffu));
+    unsigned mine_p = 0xffffffffu, mine_k = 0xffffffffu;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const unsigned r = static_cast<unsigned>(lane + 32 * q);
+      if (pos[q] == ppos) mine_p = r;
+      if (pos[q] == k) mine_k = r;
+    }
+    const int rp = static_cast<int>(__reduce_min_sync(0xffffffffu, mine_p));   // pivot row
+    const int rk = static_cast<int>(__reduce_min_sync(0xffffffffu, mine_k));   // row at k
+    const int owner = rp & 31, qp = rp >> 5;
+    double prow[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      double sel = pan[0][c];
+#pragma unroll
+      for (int q = 1; q < R; ++q) sel = (qp == q) ? pan[q][c] : sel;
+      prow[c] = __shfl_sync(0xffffffffu, sel, owner);
+    }
+    const double piv = prow[kk];
+    if (!(fabs(piv) >= 1e-12 * rs[rp])) return VK_PATCH_SMALL_PIVOT;   // warp-uniform
+    const double rinv = 1.0 / piv;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) prow[c] = (c == kk) ? rinv : prow[c] * rinv;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int r = lane + 32 * q;
+      if (r == rp) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) pan[q][c] = prow[c];
+        pos[q] = k;
+      } else {
+        const double f = pan[q][kk];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) pan[q][c] = (c == kk) ? -f * rinv : fma(-f, prow[c], pan[q][c]);
+        if (r == rk) pos[q] = ppos;
+      }
+    }
+    if (lane == 0) pids[kk] = rp;
+  }
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int r = lane + 32 * q;
+    if (r < S) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        W[r * LD + k0 + c] = pan[q][c];
+        Pb[r * NB + c] = pan[q][c];
+      }
+    }
+  }
+  __syncwarp();
+  if (lane < NB) isp[pids[lane]] = 1;
+  return VK_PATCH_OK;
+}
+
+#ifdef VK_FACTOR_TRACE
+#define VK_TRACE_ADD(slot, t0) (trc[slot] += clock64() - (t0))
+#else
+#define VK_TRACE_ADD(slot, t0)
+#endif
+
+template <int S>
+__global__ void __launch_bounds__(256, (S <= 96) ? 2 : 1) factor_dmma_kernel(
+    const int* __restrict__ plist, int count, const int64_t* __restrict__ off,
+    const int* __restrict__ idx, const int* __restrict__ ptr, const int* __restrict__ col,
+    const double* __restrict__ val, const int64_t* __restrict__ opoff, double* __restrict__ inv,
+    int* __restrict__ status) {
+  constexpr int NT = 256, NW = NT / 32, LD = S + 1, NB = 8, TT = S / 8, R = (S + 31) / 32;
+  static_assert(S % 8 == 0, "8x8 tiles");
+  extern __shared__ __align__(16) double smem[];
+  double* W = smem;                                  // S x LD
+  double* Pb0 = W + S * LD;                          // 2 x (S x NB)  factored panels
+  double* Rb0 = Pb0 + 2 * S * NB;                    // 2 x (NB x LD) pivot rows
+  double* rs = Rb0 + 2 * NB * LD;                    // S row scales
+  int* sidx = reinterpret_cast<int*>(rs + S);        // S
+  int* rowoff = sidx + S;                            // S + 1
+  int* rowk0 = rowoff + S + 1;                       // S
+  int* perm = rowk0 + S;                             // S  position -> row
+  int* posof = perm + S;                             // S  row -> position
+  int* isp0 = posof + S;                             // 2 x S pivot-row flags
+  __shared__ int pids0[2][NB];
+  __shared__ int s_bad;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+#ifdef VK_FACTOR_TRACE
+  long long trc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tt0;
+#endif
+
+  for (int bb = blockIdx.x; bb < count; bb += gridDim.x) {
+#ifdef VK_FACTOR_TRACE
+    tt0 = clock64();
+#endif
+    const int p = plist[bb];
+    const int64_t base = off[p];
+    const int s = static_cast<int>(off[p + 1] - base);
+    const int np = (s + NB - 1) / NB;
+    for (int i = t; i < S; i += NT) {
+      if (i < s) {
+        const int r = idx[base + i];
+        sidx[i] = r;
+        const int a0 = ptr[r];
+        rowk0[i] = a0;
+        rowoff[i + 1] = ptr[r + 1] - a0;
+      }
+      isp0[i] = 0;
+      isp0[S + i] = 0;
+    }
+    for (int e = t; e < S * LD; e += NT) W[e] = 0.0;
+    if (t == 0) s_bad = 0;
+    __syncthreads();
+    if (warp == 0) warp_scan_rows(lane, s, rowoff);
+    __syncthreads();
+    extract_entries(t, NT, s, LD, sidx, rowoff, rowk0, col, val, W);
+    for (int i = s + t; i < S; i += NT) W[i * LD + i] = 1.0;       // identity tail
+    __syncthreads();
+    for (int i = warp; i < S; i += NW) {                           // row scales, zero-row guard
+      double m = 0.0;
+      for (int j = lane; j < S; j += 32) m = fmax(m, fabs(W[i * LD + j]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) {
+        rs[i] = m;
+        if (i < s && m == 0.0) s_bad = VK_PATCH_ZERO_ROW;
+      }
+    }
+    __syncthreads();
+    VK_TRACE_ADD(0, tt0);
+    if (s_bad) {
+      if (t == 0) status[p] = s_bad;
+      __syncthreads();
+      continue;
+    }
+    // positions of rows lane + 32q, kept by warp 0 for the whole patch
+    int pos[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) pos[q] = (lane + 32 * q < S) ? lane + 32 * q : 0x7fffffff;
+#ifdef VK_FACTOR_TRACE
+    tt0 = clock64();
+#endif
+    // prologue: panel 0, its pivot rows
+    if (warp == 0) {
+      const int st = factor_panel<S, R>(W, Pb0, pos, isp0, pids0[0], rs, 0, lane);
+      if (st && lane == 0) s_bad = st;
+    }
+    __syncthreads();
+    if (!s_bad)
+      for (int e = t; e < NB * S; e += NT) Rb0[(e / S) * LD + e % S] = W[pids0[0][e / S] * LD + e % S];
+    __syncthreads();
+    VK_TRACE_ADD(1, tt0);
+    for (int pp = 0; pp < np && !s_bad; ++pp) {
+      const int cur = pp & 1, nxt = cur ^ 1;
+      const double* Pb = Pb0 + cur * S * NB;
+      const double* Rb = Rb0 + cur * NB * LD;
+      const int* isp = isp0 + cur * S;
+      const bool ahead = pp + 1 < np;
+#ifdef VK_FACTOR_TRACE
+      tt0 = clock64();
+#endif
+      if (warp == 0) {
+        if (ahead) {
+          // look-ahead: panel pp+1's own column tile first, then factor it
+          for (int ti = 0; ti < TT; ++ti) panel_update_tile(W, LD, Pb, Rb, isp, ti, pp + 1, lane);
+          __syncwarp();
+          VK_TRACE_ADD(2, tt0);
+#ifdef VK_FACTOR_TRACE
+          tt0 = clock64();
+#endif
+          const int st = factor_panel<S, R>(W, Pb0 + nxt * S * NB, pos, isp0 + nxt * S,
+                                            pids0[nxt], rs, (pp + 1) * NB, lane);
+          if (st && lane == 0) s_bad = st;
+          VK_TRACE_ADD(3, tt0);
+        }
+      } else {
+        // warps 1..7: every other column tile except panels pp and pp+1
+        for (int tile = warp - 1; tile < TT * TT; tile += NW - 1) {
+          const int ti = tile % TT, tj = tile / TT;
+          if (tj == pp || (ahead && tj == pp + 1)) continue;
+          panel_update_tile(W, LD, Pb, Rb, isp, ti, tj, lane);
+        }
+        VK_TRACE_ADD(4, tt0);
+      }
+#ifdef VK_FACTOR_TRACE
+      tt0 = clock64();
+#endif
+      __syncthreads();
+      VK_TRACE_ADD(5, tt0);
+#ifdef VK_FACTOR_TRACE
+      tt0 = clock64();
+#endif
+      if (s_bad) break;                                // block-uniform
+      if (t < NB) isp0[cur * S + pids0[cur][t]] = 0;   // panel pp done
+      if (ahead)                                       // pivot rows of pp+1, fully updated
+        for (int e = t; e < NB * S; e += NT)
+          Rb0[nxt * NB * LD + (e / S) * LD + e % S] = W[pids0[nxt][e / S] * LD + e % S];
+      __syncthreads();
+      VK_TRACE_ADD(6, tt0);
+    }
+    if (s_bad) {
+      if (t == 0) status[p] = s_bad;
+      __syncthreads();
+      continue;
+    }
+#ifdef VK_FACTOR_TRACE
+    tt0 = clock64();
+#endif
+    if (warp == 0) {                                   // row <-> position maps
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int r = lane + 32 * q;
+        if (r < S) {
+          posof[r] = pos[q];
+          perm[pos[q]] = r;
+        }
+      }
+    }
+    __syncthreads();
+    // inverse, column-major, coalesced: Ainv[i][j] = W[perm[i]][posof[j]]
+    // (the mapping of the unblocked kernels, dst[perm[pc] s + posof[pr]])
+    double* dst = inv + opoff[p];
+    for (int e = t; e < s * s; e += NT) {
+      const int j = e / s, i = e % s;
+      dst[e] = W[perm[i] * LD + posof[j]];
+    }
+    if (t == 0) status[p] = VK_PATCH_OK;
+    __syncthreads();
+    VK_TRACE_ADD(7, tt0);
+  }
+#ifdef VK_FACTOR_TRACE
+  if (blockIdx.x == 0 && (t == 0 || t == 32))
+    printf("[dmma S=%d t=%d] init+extract %lld prologue %lld w0-tile %lld w0-panel %lld "
+           "upd %lld bar1 %lld rcopy+bar2 %lld scatter %lld (cycles, summed over patches)\n",
+           S, t, trc[0], trc[1], trc[2], trc[3], trc[4], trc[5], trc[6], trc[7]);
+#endif
+}
+
+// VK_FACTOR_DMMA=0 keeps the register-tiled kernel for the large classes
+bool dmma_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("VK_FACTOR_DMMA");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 struct Bucket {
   int smax;
   std::vector<int> ids;
 };
 
 std::vector<Bucket> make_buckets(const std::vector<int64_t>& off, int first, int count) {
-  static const int edges[] = {16, 24, 32, 40, 48, 56, 64, 80, 96, 112, 128, 144, kMaxPatch};
+  static const int edges[] = {16, 24, 32, 40, 48, 56, 64, 80, 96, 104, 112, 128, 144, kMaxPatch};
   std::vector<Bucket> b(sizeof(edges) / sizeof(int));
   for (size_t i = 0; i < b.size(); ++i) b[i].smax = edges[i];
   for (int p = first; p < first + count; ++p) {
@@ -549,7 +886,29 @@ int launch_class(int smax, const int* d_ids, int count, const vk_patches_s* h, c
                  cudaStream_t st) {
   if (count == 0) return VK_OK;
   const size_t smem = factor_smem_bytes(smax);
-  if (!extract_only && smax <= 128) {
+  if (!extract_only && smax > 64 && smax <= 128 && dmma_enabled()) {
+    cudaError_t e = cudaSuccess;
+#define VK_DMMA(S_)                                                                             \
+  do {                                                                                          \
+    auto kern = factor_dmma_kernel<S_>;                                                         \
+    const size_t dsm = dmma_smem_bytes<S_>();                                                   \
+    e = vk_smem_optin((const void*)kern, int(dsm));                                             \
+    const int grid = std::max(1, std::min(count, vk_resident_blocks((const void*)kern, 256, dsm))); \
+    if (e == cudaSuccess)                                                                       \
+      kern<<<grid, 256, dsm, st>>>(d_ids, count, h->off, h->idx, a->indptr, a->indices,          \
+                                   a->data, h->opoff, h->inv, d_status);                        \
+  } while (0)
+    if (smax <= 80) VK_DMMA(80);
+    else if (smax <= 96) VK_DMMA(96);
+    else if (smax <= 104) VK_DMMA(104);
+    else if (smax <= 112) VK_DMMA(112);
+    else VK_DMMA(128);
+#undef VK_DMMA
+    if (e != cudaSuccess) {
+      vk::set_error("factor_dmma_kernel: %s", cudaGetErrorString(e));
+      return VK_ERR_CUDA;
+    }
+  } else if (!extract_only && smax <= 128) {
     // register-tiled classes: (TR x TC threads, RA x CB tile per thread)
     cudaError_t e = cudaSuccess;
 #define VK_TILE(TR_, TC_, RA_, CB_, MB_)                                                         \
