@@ -328,22 +328,42 @@ __host__ __device__ constexpr size_t dmma_smem_bytes() {
          sizeof(int) * (7 * size_t(S) + 1);
 }
 
-// one 8x8 tile of the panel update: C = (pivot row ? 0 : C) + Pn R
-__device__ __forceinline__ void panel_update_tile(double* W, int LD, const double* Pb,
-                                                  const double* Rb, const int* isp, int ti, int tj,
-                                                  int lane) {
-  const int row = ti * 8 + (lane >> 2);
-  const int cc = tj * 8 + 2 * (lane & 3);
-  const bool zr = isp[row] != 0;
-  double c0 = zr ? 0.0 : W[row * LD + cc];
-  double c1 = zr ? 0.0 : W[row * LD + cc + 1];
-  const double a0 = Pb[row * 8 + (lane & 3)], a1 = Pb[row * 8 + 4 + (lane & 3)];
-  const double b0 = Rb[(lane & 3) * LD + tj * 8 + (lane >> 2)];
-  const double b1 = Rb[(4 + (lane & 3)) * LD + tj * 8 + (lane >> 2)];
-  dmma_8x8x4(c0, c1, a0, b0);
-  dmma_8x8x4(c0, c1, a1, b1);
-  W[row * LD + cc] = c0;
-  W[row * LD + cc + 1] = c1;
+// up to B 8x8 tiles of the panel update at once (all shared-memory loads
+// first, then the 8 DMMAs, then the stores: the tiles' dependency chains
+// overlap instead of running back to back); tiles (ti[u], tj[u]), u < n
+template <int B>
+__device__ __forceinline__ void panel_update_tiles(double* W, int LD, const double* Pb,
+                                                   const double* Rb, const int* isp,
+                                                   const int (&ti)[B], const int (&tj)[B],
+                                                   const bool (&ok)[B], int lane) {
+  double c0[B], c1[B], a0[B], a1[B], b0[B], b1[B];
+  int row[B], cc[B];
+#pragma unroll
+  for (int u = 0; u < B; ++u) {
+    row[u] = ti[u] * 8 + (lane >> 2);
+    cc[u] = tj[u] * 8 + 2 * (lane & 3);
+    if (ok[u]) {
+      const bool zr = isp[row[u]] != 0;
+      c0[u] = zr ? 0.0 : W[row[u] * LD + cc[u]];
+      c1[u] = zr ? 0.0 : W[row[u] * LD + cc[u] + 1];
+      a0[u] = Pb[row[u] * 8 + (lane & 3)];
+      a1[u] = Pb[row[u] * 8 + 4 + (lane & 3)];
+      b0[u] = Rb[(lane & 3) * LD + tj[u] * 8 + (lane >> 2)];
+      b1[u] = Rb[(4 + (lane & 3)) * LD + tj[u] * 8 + (lane >> 2)];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < B; ++u)
+    if (ok[u]) dmma_8x8x4(c0[u], c1[u], a0[u], b0[u]);
+#pragma unroll
+  for (int u = 0; u < B; ++u)
+    if (ok[u]) dmma_8x8x4(c0[u], c1[u], a1[u], b1[u]);
+#pragma unroll
+  for (int u = 0; u < B; ++u)
+    if (ok[u]) {
+      W[row[u] * LD + cc[u]] = c0[u];
+      W[row[u] * LD + cc[u] + 1] = c1[u];
+    }
 }
 
 // warp 0: the 8 Gauss-Jordan steps of the panel at k0 (columns k0..k0+7 of
@@ -450,6 +470,8 @@ __global__ void __launch_bounds__(256, (S <= 96) ? 2 : 1) factor_dmma_kernel(
     const double* __restrict__ val, const int64_t* __restrict__ opoff, double* __restrict__ inv,
     int* __restrict__ status) {
   constexpr int NT = 256, NW = NT / 32, LD = S + 1, NB = 8, TT = S / 8, R = (S + 31) / 32;
+  constexpr int TB = (S <= 96) ? 1 : 4;              // tiles per batch (register budget:
+                                                     // 2 CTAs / SM below 97)
   static_assert(S % 8 == 0, "8x8 tiles");
   extern __shared__ __align__(16) double smem[];
   double* W = smem;                                  // S x LD
@@ -543,7 +565,17 @@ __global__ void __launch_bounds__(256, (S <= 96) ? 2 : 1) factor_dmma_kernel(
       if (warp == 0) {
         if (ahead) {
           // look-ahead: panel pp+1's own column tile first, then factor it
-          for (int ti = 0; ti < TT; ++ti) panel_update_tile(W, LD, Pb, Rb, isp, ti, pp + 1, lane);
+          for (int t0 = 0; t0 < TT; t0 += TB) {
+            int ti[TB], tj[TB];
+            bool ok[TB];
+#pragma unroll
+            for (int u = 0; u < TB; ++u) {
+              ti[u] = t0 + u;
+              tj[u] = pp + 1;
+              ok[u] = t0 + u < TT;
+            }
+            panel_update_tiles<TB>(W, LD, Pb, Rb, isp, ti, tj, ok, lane);
+          }
           __syncwarp();
           VK_TRACE_ADD(2, tt0);
 #ifdef VK_FACTOR_TRACE
@@ -556,10 +588,17 @@ __global__ void __launch_bounds__(256, (S <= 96) ? 2 : 1) factor_dmma_kernel(
         }
       } else {
         // warps 1..7: every other column tile except panels pp and pp+1
-        for (int tile = warp - 1; tile < TT * TT; tile += NW - 1) {
-          const int ti = tile % TT, tj = tile / TT;
-          if (tj == pp || (ahead && tj == pp + 1)) continue;
-          panel_update_tile(W, LD, Pb, Rb, isp, ti, tj, lane);
+        for (int m0 = warp - 1; m0 < TT * TT; m0 += TB * (NW - 1)) {
+          int ti[TB], tj[TB];
+          bool ok[TB];
+#pragma unroll
+          for (int u = 0; u < TB; ++u) {
+            const int tile = m0 + u * (NW - 1);
+            ti[u] = tile % TT;
+            tj[u] = tile / TT;
+            ok[u] = tile < TT * TT && tj[u] != pp && !(ahead && tj[u] == pp + 1);
+          }
+          panel_update_tiles<TB>(W, LD, Pb, Rb, isp, ti, tj, ok, lane);
         }
         VK_TRACE_ADD(4, tt0);
       }
