@@ -588,6 +588,14 @@ __global__ void __launch_bounds__(256, (S <= 96) ? 2 : 1) factor_dmma_kernel(
         }
       } else {
         // warps 1..7: every other column tile except panels pp and pp+1
+        if constexpr (TB == 1) {
+          for (int tile = warp - 1; tile < TT * TT; tile += NW - 1) {
+            const int ti[1] = {tile % TT}, tj[1] = {tile / TT};
+            if (tj[0] == pp || (ahead && tj[0] == pp + 1)) continue;
+            const bool ok[1] = {true};
+            panel_update_tiles<1>(W, LD, Pb, Rb, isp, ti, tj, ok, lane);
+          }
+        } else
         for (int m0 = warp - 1; m0 < TT * TT; m0 += TB * (NW - 1)) {
           int ti[TB], tj[TB];
           bool ok[TB];
