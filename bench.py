@@ -62,6 +62,12 @@ def workload(cfg):
             "every patch per step, seeded uniform[-1,1] residual")
 
 
+# (case, k, coarse cells per side, refinements) of each config's hierarchy
+# and the reference's setup time
+SETUP_SPEC = {"cfg2": ("th-tri", 2, 16, 4), "cfg3": ("th-tri", 4, 16, 3),
+              "cfg4": ("th-quad", 3, 16, 3), "cfg5": ("bdm", 3, 16, 3)}
+REF_SETUP_S = {"cfg2": 163.9, "cfg3": 193.3, "cfg4": 108.5, "cfg5": 154.5}
+
 METRIC = "Vanka sweep patch-solves/s (P4/P3 128x128 finest level, damping 0.5)"
 UNIT = "patch-solves/s"
 CPU_SAMPLE_PER_WORKER = 2048   # ours-arm cpu_baseline: bounded sample per host core
@@ -533,12 +539,46 @@ class Level:
                 "coarse_inverse": {"n": n0, "ms": t_c * 1e3,
                                    "tflops": 2.0 * n0 ** 3 / t_c / 1e12}}
 
+    def device_setup(self):
+        """The whole hierarchy built on the device from scratch (meshes / DoF
+        maps on the host; assembly, prolongations, patches, factorisation,
+        coarse inverse on the device) — SURVEY §8(f) 3-4 — timed against the
+        reference's setup, and its MG-FGMRES iterations."""
+        import torch
+        import paper_2409_14222_b200 as V
+        from paper_2409_14222_b200 import mg
+        from paper_2409_14222_b200.solver import FgmresSolver, mg_rhs
+        case, k, n0, refs = SETUP_SPEC[self.cfg]
+        old = mg.COARSE_CELLS_PER_SIDE
+        mg.COARSE_CELLS_PER_SIDE = n0
+        try:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            hier = V.build_hierarchy(case, k, refs, nu=2, damping=0.5)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+        finally:
+            mg.COARSE_CELLS_PER_SIDE = old
+        _, its, conv, hist = FgmresSolver(hier).solve(
+            torch.from_numpy(mg_rhs(self.pack)).to(self.dev))
+        rel, ref_its = _history_rel(self.cfg, hist)
+        del hier
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        return {"build_hierarchy_s": dt, "reference_setup_s": REF_SETUP_S.get(self.cfg),
+                "iterations": its, "reference_iterations": ref_its, "converged": bool(conv),
+                "history_max_rel_vs_reference": rel,
+                "note": "device assembly of every level's operator + prolongations + patches "
+                        "+ factorisation + coarse inverse (no pack); reference setup time "
+                        "survey-measured (SURVEY.md §6)"}
+
     def full_entry(self, steps, peak):
         out = {"workload": workload(self.cfg), "sweep": self.sweep_entry(steps, peak)}
         out["mg_fgmres"] = self.tts()
         out["residual_spmv"] = self.residual(peak)
         out["transfers"] = self.transfers(peak)
         out["factor"] = self.factor()
+        out["device_setup"] = self.device_setup()
         return out
 
     def close(self):

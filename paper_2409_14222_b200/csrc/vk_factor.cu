@@ -375,6 +375,9 @@ template <int S, int R>
 __device__ __forceinline__ int factor_panel(double* W, double* Pb, int (&pos)[R], int* isp,
                                             int* pids, const double* rs, int k0, int lane) {
   constexpr int LD = S + 1, NB = 8;
+  bool bad = false;   // no early exit: the 8 steps stay straight-line code, so
+                      // the compiler can overlap step k+1's reductions with
+                      // the tail of step k (a failed guard only flags the patch)
   double pan[R][NB];
 #pragma unroll
   for (int q = 0; q < R; ++q) {
@@ -421,8 +424,8 @@ __device__ __forceinline__ int factor_panel(double* W, double* Pb, int (&pos)[R]
       prow[c] = __shfl_sync(0xffffffffu, sel, owner);
     }
     const double piv = prow[kk];
-    if (!(fabs(piv) >= 1e-12 * rs[rp])) return VK_PATCH_SMALL_PIVOT;   // warp-uniform
-    const double rinv = 1.0 / piv;
+    bad |= !(fabs(piv) >= 1e-12 * rs[rp]);           // warp-uniform
+    const double rinv = __drcp_rn(piv);              // == 1.0 / piv (correctly rounded)
 #pragma unroll
     for (int c = 0; c < NB; ++c) prow[c] = (c == kk) ? rinv : prow[c] * rinv;
 #pragma unroll
@@ -453,6 +456,7 @@ __device__ __forceinline__ int factor_panel(double* W, double* Pb, int (&pos)[R]
     }
   }
   __syncwarp();
+  if (bad) return VK_PATCH_SMALL_PIVOT;
   if (lane < NB) isp[pids[lane]] = 1;
   return VK_PATCH_OK;
 }
