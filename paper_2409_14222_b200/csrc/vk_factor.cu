@@ -428,19 +428,19 @@ __device__ __forceinline__ int factor_panel(double* W, double* Pb, int (&pos)[R]
     const double rinv = __drcp_rn(piv);              // == 1.0 / piv (correctly rounded)
 #pragma unroll
     for (int c = 0; c < NB; ++c) prow[c] = (c == kk) ? rinv : prow[c] * rinv;
+    // branch-free: the pivot row takes the scaled row, every other row the
+    // elimination (no divergence between the owner lane and the rest)
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       const int r = lane + 32 * q;
-      if (r == rp) {
+      const bool isp_row = (r == rp);
+      const double f = pan[q][kk];
 #pragma unroll
-        for (int c = 0; c < NB; ++c) pan[q][c] = prow[c];
-        pos[q] = k;
-      } else {
-        const double f = pan[q][kk];
-#pragma unroll
-        for (int c = 0; c < NB; ++c) pan[q][c] = (c == kk) ? -f * rinv : fma(-f, prow[c], pan[q][c]);
-        if (r == rk) pos[q] = ppos;
+      for (int c = 0; c < NB; ++c) {
+        const double e = (c == kk) ? -f * rinv : fma(-f, prow[c], pan[q][c]);
+        pan[q][c] = isp_row ? prow[c] : e;
       }
+      pos[q] = isp_row ? k : ((r == rk) ? ppos : pos[q]);
     }
     if (lane == 0) pids[kk] = rp;
   }
