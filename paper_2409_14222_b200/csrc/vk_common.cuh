@@ -33,6 +33,7 @@ struct Csr {
   // CSR-stream schedule: row blocks of <= kStreamNnz nonzeros / kStreamRows rows
   int32_t nblocks = 0;
   int2* blk = nullptr;         // [nblocks+1] (first row, first nonzero) of each block
+  uint64_t uid = 0;            // process-unique id of this (immutable) sparsity pattern
 };
 
 #ifndef VK_STREAM_THREADS
@@ -74,6 +75,12 @@ struct Patches {
   // patch ids grouped by size class, and (smax, first, count) per class
   int32_t* fac_ids = nullptr;
   int32_t* fac_status = nullptr;  // [npatch]
+  // extraction map, built by the first factorisation against a matrix: for
+  // every (patch row, stored CSR entry of that row) the local column (-1 if
+  // the column is not in the patch); keyed by the CSR handle (its pattern)
+  int64_t* fac_eoff = nullptr;    // [npatch+1] offsets into fac_emap
+  int16_t* fac_emap = nullptr;
+  uint64_t fac_emap_key = 0;      // Csr::uid the map was built for (0 = none)
   std::vector<std::tuple<int, int, int>> fac_classes;
 };
 

@@ -1,3 +1,4 @@
+#include <atomic>
 // K5/K6: CSR matrices on the device, SpMV / fused residual / transfers.
 //
 // Replaces scipy csr_matvec at reference sparsela.py:45-47 (spmv),
@@ -443,7 +444,9 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
   }
   VK_REQUIRE(hp[0] == 0 && hp[nrows] == nnz, "vk_csr_create: indptr does not match nnz");
   auto rb = make_row_blocks(hp);
+  static std::atomic<uint64_t> next_uid{1};
   auto* a = new vk_csr_s();
+  a->uid = next_uid.fetch_add(1);
   a->nrows = nrows;
   a->ncols = ncols;
   a->nnz = nnz;

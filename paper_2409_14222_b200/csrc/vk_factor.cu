@@ -27,6 +27,8 @@
 #include <mutex>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "vk_common.cuh"
 
 namespace {
@@ -95,6 +97,72 @@ __device__ __forceinline__ void extract_entries(int tid, int nth, int s, int ld,
         if (sidx[mid] < c[u]) lo = mid + 1; else hi = mid;
       }
       if (sidx[lo] == c[u]) A[rw[u] * ld + lo] = v[u];
+    }
+  }
+}
+
+// Extraction through the cached map (re-factorisations): warp per patch row,
+// lanes over the row's stored entries; the local column comes from the map,
+// so no searches — a streaming gather of the values (bit-exact copy).
+__device__ __forceinline__ void extract_rows_mapped(int warp, int lane, int nw, int s, int ld,
+                                                    const int* rowoff, const int* rowk0,
+                                                    const double* __restrict__ val,
+                                                    const int16_t* __restrict__ emap,
+                                                    double* A) {
+  for (int i = warp; i < s; i += nw) {
+    const int e0 = rowoff[i], len = rowoff[i + 1] - e0, k0 = rowk0[i];
+    for (int kk = lane; kk < len; kk += 64) {
+      const int j0 = __ldg(emap + e0 + kk);
+      const double v0 = __ldg(val + k0 + kk);
+      const bool two = kk + 32 < len;
+      const int j1 = two ? __ldg(emap + e0 + kk + 32) : -1;
+      const double v1 = two ? __ldg(val + k0 + kk + 32) : 0.0;
+      if (j0 >= 0) A[i * ld + j0] = v0;
+      if (j1 >= 0) A[i * ld + j1] = v1;
+    }
+  }
+}
+
+// per patch: number of stored CSR entries in its rows (map size)
+__global__ void entry_count_kernel(int npatch, const int64_t* __restrict__ off,
+                                   const int* __restrict__ idx, const int* __restrict__ ptr,
+                                   int64_t* __restrict__ cnt) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npatch; p += gridDim.x * blockDim.x) {
+    int64_t c = 0;
+    for (int64_t q = off[p]; q < off[p + 1]; ++q) c += ptr[idx[q] + 1] - ptr[idx[q]];
+    cnt[p + 1] = c;
+  }
+}
+
+// per patch (one warp): the local column of every stored entry of its rows
+// (binary search in the sorted patch list, as extract_entries), or -1
+__global__ void __launch_bounds__(128) emap_fill_kernel(int npatch, const int64_t* __restrict__ off,
+                                                        const int* __restrict__ idx,
+                                                        const int* __restrict__ ptr,
+                                                        const int* __restrict__ col,
+                                                        const int64_t* __restrict__ eoff,
+                                                        int16_t* __restrict__ emap) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int p = gw; p < npatch; p += nw) {
+    const int64_t base = off[p];
+    const int s = static_cast<int>(off[p + 1] - base);
+    const int* sidx = idx + base;
+    int64_t e = eoff[p];
+    for (int i = 0; i < s; ++i) {
+      const int r = __ldg(sidx + i);
+      const int a0 = __ldg(ptr + r), len = __ldg(ptr + r + 1) - a0;
+      for (int kk = lane; kk < len; kk += 32) {
+        const int c = __ldg(col + a0 + kk);
+        int lo = 0, hi = s - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (__ldg(sidx + mid) < c) lo = mid + 1; else hi = mid;
+        }
+        emap[e + kk] = (__ldg(sidx + lo) == c) ? static_cast<int16_t>(lo) : int16_t(-1);
+      }
+      e += len;
     }
   }
 }
@@ -472,7 +540,8 @@ __global__ void __launch_bounds__(256, (S <= 96) ? 2 : 1) factor_dmma_kernel(
     const int* __restrict__ plist, int count, const int64_t* __restrict__ off,
     const int* __restrict__ idx, const int* __restrict__ ptr, const int* __restrict__ col,
     const double* __restrict__ val, const int64_t* __restrict__ opoff, double* __restrict__ inv,
-    int* __restrict__ status) {
+    int* __restrict__ status, const int64_t* __restrict__ eoff,
+    const int16_t* __restrict__ emap) {
   constexpr int NT = 256, NW = NT / 32, LD = S + 1, NB = 8, TT = S / 8, R = (S + 31) / 32;
   constexpr int TB = (S <= 96) ? 1 : 4;              // tiles per batch (register budget:
                                                      // 2 CTAs / SM below 97)
@@ -520,7 +589,10 @@ __global__ void __launch_bounds__(256, (S <= 96) ? 2 : 1) factor_dmma_kernel(
     __syncthreads();
     if (warp == 0) warp_scan_rows(lane, s, rowoff);
     __syncthreads();
-    extract_entries(t, NT, s, LD, sidx, rowoff, rowk0, col, val, W);
+    if (emap)
+      extract_rows_mapped(warp, lane, NW, s, LD, rowoff, rowk0, val, emap + eoff[p], W);
+    else
+      extract_entries(t, NT, s, LD, sidx, rowoff, rowk0, col, val, W);
     for (int i = s + t; i < S; i += NT) W[i * LD + i] = 1.0;       // identity tail
     __syncthreads();
     for (int i = warp; i < S; i += NW) {                           // row scales, zero-row guard
@@ -722,7 +794,8 @@ __global__ void __launch_bounds__(TR * TC, MB) factor_tile_kernel(
     const int* __restrict__ plist, int count, const int64_t* __restrict__ off,
     const int* __restrict__ idx, const int* __restrict__ ptr, const int* __restrict__ col,
     const double* __restrict__ val, const int64_t* __restrict__ opoff, double* __restrict__ inv,
-    int* __restrict__ status) {
+    int* __restrict__ status, const int64_t* __restrict__ eoff,
+    const int16_t* __restrict__ emap) {
   constexpr int NT = TR * TC;
   constexpr int NW = NT / 32;
   constexpr int SM = TR * RA;              // largest block (rows)
@@ -763,7 +836,10 @@ __global__ void __launch_bounds__(TR * TC, MB) factor_tile_kernel(
     __syncthreads();
     if (t < 32) warp_scan_rows(lane, s, rowoff);
     __syncthreads();
-    extract_entries(t, NT, s, ld, sidx, rowoff, rowk0, col, val, A);
+    if (emap)
+      extract_rows_mapped(warp, lane, NW, s, ld, rowoff, rowk0, val, emap + eoff[p], A);
+    else
+      extract_entries(t, NT, s, ld, sidx, rowoff, rowk0, col, val, A);
     __syncthreads();
     for (int i = t; i < s; i += NT) {           // row scales, zero-row guard
       double m = 0.0;
@@ -947,7 +1023,8 @@ int launch_class(int smax, const int* d_ids, int count, const vk_patches_s* h, c
     const int grid = std::max(1, std::min(count, vk_resident_blocks((const void*)kern, 256, dsm))); \
     if (e == cudaSuccess)                                                                       \
       kern<<<grid, 256, dsm, st>>>(d_ids, count, h->off, h->idx, a->indptr, a->indices,          \
-                                   a->data, h->opoff, h->inv, d_status);                        \
+                                   a->data, h->opoff, h->inv, d_status, h->fac_eoff,            \
+                                   h->fac_emap);                                                \
   } while (0)
     if (smax <= 80) VK_DMMA(80);
     else if (smax <= 96) VK_DMMA(96);
@@ -972,7 +1049,8 @@ int launch_class(int smax, const int* d_ids, int count, const vk_patches_s* h, c
     const int grid = std::max(1, std::min(count, 148 * std::max(per_sm, 1)));                 \
     if (e == cudaSuccess)                                                                      \
       kern<<<grid, TR_ * TC_, dsm, st>>>(d_ids, count, h->off, h->idx, a->indptr, a->indices,  \
-                                         a->data, h->opoff, h->inv, d_status);                 \
+                                         a->data, h->opoff, h->inv, d_status, h->fac_eoff,     \
+                                         h->fac_emap);                                         \
   } while (0)
     // MB: CTAs per SM the register budget must allow (occupancy vs. spills,
     // measured per class)
@@ -1139,6 +1217,35 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
     VK_CHECK_CUDA(cudaMalloc(&h->fac_status, sizeof(int32_t) * std::max(h->npatch, 1)));
   }
   int* d_status = h->fac_status;
+  // extraction map for this matrix (first factorisation against it): later
+  // factorisations gather the block entries without searching
+  if (h->fac_emap_key != a->uid && h->npatch > 0) {
+    cudaFree(h->fac_emap);
+    h->fac_emap = nullptr;
+    h->fac_emap_key = 0;
+    if (!h->fac_eoff) VK_CHECK_CUDA(cudaMalloc(&h->fac_eoff, sizeof(int64_t) * (h->npatch + 1)));
+    VK_CHECK_CUDA(cudaMemset(h->fac_eoff, 0, sizeof(int64_t) * (h->npatch + 1)));
+    entry_count_kernel<<<vk_grid(h->npatch, 256), 256>>>(h->npatch, h->off, h->idx, a->indptr,
+                                                        h->fac_eoff);
+    VK_CHECK_LAUNCH();
+    size_t tb = 0;
+    VK_CHECK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, h->fac_eoff, h->fac_eoff,
+                                                h->npatch + 1));
+    void* tmp = nullptr;
+    VK_CHECK_CUDA(cudaMalloc(&tmp, std::max<size_t>(tb, 1)));
+    cudaError_t se = cub::DeviceScan::InclusiveSum(tmp, tb, h->fac_eoff, h->fac_eoff,
+                                                   h->npatch + 1);
+    cudaFree(tmp);
+    VK_CHECK_CUDA(se);
+    int64_t etotal = 0;
+    VK_CHECK_CUDA(cudaMemcpy(&etotal, h->fac_eoff + h->npatch, sizeof(int64_t),
+                             cudaMemcpyDeviceToHost));
+    VK_CHECK_CUDA(cudaMalloc(&h->fac_emap, sizeof(int16_t) * std::max<int64_t>(etotal, 1)));
+    emap_fill_kernel<<<vk_grid(int64_t(h->npatch) * 32, 128, 148 * 16), 128>>>(
+        h->npatch, h->off, h->idx, a->indptr, a->indices, h->fac_eoff, h->fac_emap);
+    VK_CHECK_LAUNCH();
+    h->fac_emap_key = a->uid;
+  }
   // The largest class (most work) runs on the legacy stream, the small ones
   // (boundary / coarse patches) beside it on an auxiliary stream; one join.
   struct AuxStream {                 // one per device (streams belong to a device)

@@ -233,6 +233,8 @@ void vk_patches_free(vk_patches_s* h) {
   cudaFree(h->zbuf);
   cudaFree(h->fac_ids);
   cudaFree(h->fac_status);
+  cudaFree(h->fac_eoff);
+  cudaFree(h->fac_emap);
   delete h;
 }
 

@@ -218,6 +218,52 @@ def test_refactor_reuses_schedule_and_tracks_values(V, name):
         assert np.array_equal((a * 0.5).view(np.uint64), h.view(np.uint64))
 
 
+@pytest.mark.parametrize("name", ["s_thtri4", "s_bdm3"])
+def test_refactor_rebuilds_extraction_map_on_new_pattern(V, name):
+    """The extraction map cached by the first factorisation (CSR entry ->
+    patch-local column) is keyed by the matrix's sparsity pattern: factoring
+    against the same values stored with extra explicit zeros (every row
+    offset shifted) must reproduce the first inverses bit for bit, and so
+    must going back to the original matrix; the inverses agree with numpy's
+    inverse of the extracted block."""
+    import scipy.sparse as sp
+    from conftest import load_case
+    from paper_2409_14222_b200.vanka import patch_inverses
+    pack, _ = load_case(name)
+    lv = pack.fine
+    a = sp.csr_matrix(lv.system.matrix)
+    ps = V.factor_patches(V.build_patches(lv.mixed, lv.system.bc), a)
+    n = ps.num_patches
+    pick = sorted({0, n // 5, n // 2, n - 1})
+    first = [patch_inverses(ps, p, 1)[0] for p in pick]
+    rng = np.random.default_rng(7)
+    coo = a.tocoo()
+    m = a.shape[0]
+    extra_r = rng.integers(0, m, 4 * m)
+    extra_c = rng.integers(0, m, 4 * m)
+    keep = a[extra_r, extra_c].A1 == 0          # only positions not yet stored
+    padded = sp.csr_matrix((np.concatenate([coo.data, np.zeros(int(keep.sum()))]),
+                            (np.concatenate([coo.row, extra_r[keep]]),
+                             np.concatenate([coo.col, extra_c[keep]]))), shape=a.shape)
+    padded.sum_duplicates()
+    padded.sort_indices()
+    assert padded.nnz > a.nnz
+    V.factor_patches(ps, padded)
+    second = [patch_inverses(ps, p, 1)[0] for p in pick]
+    V.factor_patches(ps, a)
+    third = [patch_inverses(ps, p, 1)[0] for p in pick]
+    exp = ps.export()
+    ad = a.tocsr()
+    for k, p in enumerate(pick):
+        assert np.array_equal(first[k].view(np.uint64), second[k].view(np.uint64))
+        assert np.array_equal(first[k].view(np.uint64), third[k].view(np.uint64))
+        ii = exp["indices"][exp["offsets"][p]:exp["offsets"][p + 1]]
+        blk = ad[ii][:, ii].toarray()
+        ref = np.linalg.inv(blk)
+        err = np.abs(first[k] - ref).max() / np.abs(ref).max()
+        assert err <= 1e2 * np.finfo(float).eps * np.linalg.cond(blk)
+
+
 def _uniform_patch_system(npatch, s, seed):
     """Diagonally dominant sparse matrix + `npatch` random sorted patches of
     exactly `s` DoFs (every block is nonsingular)."""
