@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvanka_b200.so")
+LIB_PATH = os.environ.get("VK_LIB") or os.path.join(_HERE, "libvanka_b200.so")  # VK_LIB: experiment builds
 
 VK_OK, VK_SINGULAR = 0, 1
 VK_ERR_ARG, VK_ERR_CUDA, VK_ERR_ALLOC, VK_ERR_UNSUPPORTED = -1, -2, -3, -4

@@ -78,7 +78,7 @@ struct Patches {
   // extraction map, built by the first factorisation against a matrix: for
   // every (patch row, stored CSR entry of that row) the local column (-1 if
   // the column is not in the patch); keyed by the CSR handle (its pattern)
-  int64_t* fac_eoff = nullptr;    // [npatch+1] offsets into fac_emap
+  int64_t* fac_eoff = nullptr;    // [total+1] offsets into fac_emap per patch row (flat idx position)
   int16_t* fac_emap = nullptr;
   uint64_t fac_emap_key = 0;      // Csr::uid the map was built for (0 = none)
   std::vector<std::tuple<int, int, int>> fac_classes;

@@ -123,15 +123,13 @@ __device__ __forceinline__ void extract_rows_mapped(int warp, int lane, int nw, 
   }
 }
 
-// per patch: number of stored CSR entries in its rows (map size)
-__global__ void entry_count_kernel(int npatch, const int64_t* __restrict__ off,
-                                   const int* __restrict__ idx, const int* __restrict__ ptr,
-                                   int64_t* __restrict__ cnt) {
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npatch; p += gridDim.x * blockDim.x) {
-    int64_t c = 0;
-    for (int64_t q = off[p]; q < off[p + 1]; ++q) c += ptr[idx[q] + 1] - ptr[idx[q]];
-    cnt[p + 1] = c;
-  }
+// per patch row (flat position g in idx): number of stored CSR entries (map
+// size); the inclusive scan gives the map offset of every patch row
+__global__ void entry_count_kernel(int64_t total, const int* __restrict__ idx,
+                                   const int* __restrict__ ptr, int64_t* __restrict__ cnt) {
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total;
+       g += int64_t(gridDim.x) * blockDim.x)
+    cnt[g + 1] = ptr[idx[g] + 1] - ptr[idx[g]];
 }
 
 // per patch (one warp): the local column of every stored entry of its rows
@@ -149,7 +147,7 @@ __global__ void __launch_bounds__(128) emap_fill_kernel(int npatch, const int64_
     const int64_t base = off[p];
     const int s = static_cast<int>(off[p + 1] - base);
     const int* sidx = idx + base;
-    int64_t e = eoff[p];
+    int64_t e = eoff[base];
     for (int i = 0; i < s; ++i) {
       const int r = __ldg(sidx + i);
       const int a0 = __ldg(ptr + r), len = __ldg(ptr + r + 1) - a0;
@@ -590,7 +588,7 @@ __global__ void __launch_bounds__(256, (S <= 96) ? 2 : 1) factor_dmma_kernel(
     if (warp == 0) warp_scan_rows(lane, s, rowoff);
     __syncthreads();
     if (emap)
-      extract_rows_mapped(warp, lane, NW, s, LD, rowoff, rowk0, val, emap + eoff[p], W);
+      extract_rows_mapped(warp, lane, NW, s, LD, rowoff, rowk0, val, emap + eoff[base], W);
     else
       extract_entries(t, NT, s, LD, sidx, rowoff, rowk0, col, val, W);
     for (int i = s + t; i < S; i += NT) W[i * LD + i] = 1.0;       // identity tail
@@ -837,7 +835,7 @@ __global__ void __launch_bounds__(TR * TC, MB) factor_tile_kernel(
     if (t < 32) warp_scan_rows(lane, s, rowoff);
     __syncthreads();
     if (emap)
-      extract_rows_mapped(warp, lane, NW, s, ld, rowoff, rowk0, val, emap + eoff[p], A);
+      extract_rows_mapped(warp, lane, NW, s, ld, rowoff, rowk0, val, emap + eoff[base], A);
     else
       extract_entries(t, NT, s, ld, sidx, rowoff, rowk0, col, val, A);
     __syncthreads();
@@ -1007,12 +1005,623 @@ __global__ void __launch_bounds__(TR * TC, MB) factor_tile_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// K2 as its own pass (default path): the dense patch blocks A[idx, idx] are
+// gathered once into the operator slots (inv + opoff[p]) that their inverses
+// will overwrite; K3 then streams each block into shared memory with one bulk
+// copy, prefetched while the previous patch is factored, so the extraction's
+// dependent global loads are off the factorisation's critical path.
+// Staged layout: row-major with stride s; for even s row i is rotated by i
+// (A[i][j] at i s + (j + i) mod s) so that lanes reading one column of
+// consecutive rows hit distinct banks (odd effective stride) in both cases.
+__host__ __device__ __forceinline__ int blk_at(int i, int j, int s) {
+  int c = j;
+  if (!(s & 1)) {
+    c = j + i;
+    if (c >= s) c -= s;
+  }
+  return i * s + c;
+}
+
+constexpr int kXRows = 8;     // patch rows per warp pass in the extraction
+constexpr int kXCols = 128;   // largest block the staged (rows / warp) kernels take
+
+// one warp per patch, kXRows rows at a time: row metadata for the pass, the
+// stored entries of every row loaded before any is placed (two per lane per
+// row in flight; longer rows finish in a second loop), the local column from
+// the extraction map, verbatim values, zeros elsewhere; rows written
+// coalesced in the staged layout.  Patches larger than kXCols are skipped
+// (their kernel extracts itself).
+__global__ void __launch_bounds__(256) extract_blocks_kernel(
+    int p0, int p1, int scut, const int64_t* __restrict__ off, const int* __restrict__ idx,
+    const int* __restrict__ ptr, const double* __restrict__ val,
+    const int64_t* __restrict__ eoff, const int16_t* __restrict__ emap,
+    const int64_t* __restrict__ opoff, int64_t obase, double* __restrict__ out) {
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) double xbuf[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* B = xbuf + warp * kXRows * kXCols;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  for (int p = p0 + blockIdx.x * (blockDim.x >> 5) + warp; p < p1; p += nw) {
+    const int64_t base = off[p];
+    const int s = static_cast<int>(off[p + 1] - base);
+    if (s > scut) continue;
+    double* o = out + (opoff[p] - obase);
+    for (int i0 = 0; i0 < s; i0 += kXRows) {
+      const int nr = min(kXRows, s - i0);
+      int a0 = 0, len = 0;
+      int64_t e0 = 0;
+      if (lane < nr) {
+        const int r = idx[base + i0 + lane];
+        e0 = eoff[base + i0 + lane];
+        a0 = ptr[r];
+        len = ptr[r + 1] - a0;
+      }
+#pragma unroll
+      for (int u = 0; u < kXRows; ++u)
+        if (u < nr)
+          for (int j = lane; j < s; j += 32) B[u * kXCols + j] = 0.0;
+      int jv[kXRows][2];
+      double vv[kXRows][2];
+#pragma unroll
+      for (int u = 0; u < kXRows; ++u) {
+        const int lu = __shfl_sync(FULL, len, u), au = __shfl_sync(FULL, a0, u);
+        const int64_t eu = __shfl_sync(FULL, e0, u);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int kk = lane + 32 * hh;
+          const bool ok = u < nr && kk < lu;
+          jv[u][hh] = ok ? __ldg(emap + eu + kk) : -1;
+          vv[u][hh] = ok ? __ldg(val + au + kk) : 0.0;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < kXRows; ++u)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+          if (jv[u][hh] >= 0) B[u * kXCols + jv[u][hh]] = vv[u][hh];
+      for (int u = 0; u < nr; ++u) {                  // rows with more than 64 entries
+        const int lu = __shfl_sync(FULL, len, u), au = __shfl_sync(FULL, a0, u);
+        const int64_t eu = __shfl_sync(FULL, e0, u);
+        for (int kk = 64 + lane; kk < lu; kk += 32) {
+          const int j = __ldg(emap + eu + kk);
+          if (j >= 0) B[u * kXCols + j] = __ldg(val + au + kk);
+        }
+      }
+      __syncwarp();
+      for (int u = 0; u < nr; ++u) {
+        const int i = i0 + u;
+        for (int j = lane; j < s; j += 32) o[blk_at(i, j, s)] = B[u * kXCols + j];
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// bulk copy of patch p's staged block (opoff slots are 16-byte aligned and
+// hold s^2 rounded up to even doubles)
+__device__ __forceinline__ void stage_block(int p, const int64_t* off, const int64_t* opoff,
+                                            const double* inv, double* stage, uint64_t* bar,
+                                            uint64_t pol) {
+  const int s = static_cast<int>(off[p + 1] - off[p]);
+  const uint32_t bytes = static_cast<uint32_t>(((s * s + 1) & ~1) * sizeof(double));
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s(stage, inv + opoff[p], bytes, bar, pol);
+}
+
+// ---------------------------------------------------------------------------
+// Rows-in-lanes Gauss-Jordan (K3, default for s <= 128).  A group of
+// NWR x CH warps factors one patch: lane l of row-warp wr owns block row
+// i = 32 wr + l, column half ch of it (C = S / CH columns) in registers, so
+// the multiplier of a row is its own register and the whole rank-1 update is
+// register DFMA with the pivot row broadcast from shared memory (LDS.128,
+// no bank conflicts).  Several patches per SM (one group per CTA) hide the
+// latency of the pivot-step chain, which the one-CTA-per-patch kernels could
+// not.
+//   * rotated columns: in the half that holds pivot column k the registers are
+//     renamed by one per step (register 0 is always column k), so the loop
+//     over k is a plain runtime loop with static register indices;
+//   * step k: the warps holding column k pick their candidate (first maximum
+//     of |a_ik| over the open positions, LAPACK idamax order, via redux.sync)
+//     and publish it with its guard verdict |a_ik| >= 1e-12 rowscale_i
+//     (sparsela.py:79-83); barrier; every warp selects the same winner, the
+//     lanes of the pivot row publish the scaled row a_r * (1/pivot); barrier;
+//     every lane updates fma(-f, p_j, a_ij) (-f/pivot in column k);
+//   * rows never move: each lane keeps its row's LAPACK position.
+// Per-element arithmetic equals the register-tiled and shared-memory kernels
+// (bit-identical inverses); the inverse is staged by position and written
+// column-major, coalesced.
+
+template <int C, int NWR, int CH, int MB>
+__global__ void __launch_bounds__(32 * NWR * CH, MB) factor_rows_kernel(
+    const int* __restrict__ plist, int count, const int64_t* __restrict__ off,
+    const int64_t* __restrict__ opoff, double* __restrict__ inv, int* __restrict__ status) {
+  constexpr int S = C * CH, NR = 32 * NWR;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int NONE = 0x7fffffff;
+  static_assert(C % 2 == 0 && NR >= S, "rows per group / column pairs");
+  extern __shared__ __align__(16) double stage[];     // the staged block (blk_at layout)
+  __shared__ __align__(16) double cb[2][NWR][C];      // candidates' scaled rows (own half)
+  __shared__ __align__(16) double ob[CH > 1 ? S : 2]; // pivot row, the other column groups
+  __shared__ double fcol[2][CH > 1 ? NR : 1];         // column k for the other groups
+  __shared__ double rsh[CH][NR];
+  __shared__ double cabs[2][NWR];                     // candidates: |value|, position, row, guard
+  __shared__ int cpos[2][NWR], crow[2][NWR], cok[2][NWR];
+  __shared__ int perm[S];
+  __shared__ int s_bad;
+  __shared__ __align__(8) uint64_t bar;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int wr = warp % NWR, ch = warp / NWR;
+  const int i = 32 * wr + lane;                       // block row of this lane
+  const uint64_t pol = evict_first_policy();          // each block is read once
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (t == 0 && static_cast<int>(blockIdx.x) < count)
+    stage_block(plist[blockIdx.x], off, opoff, inv, stage, &bar, pol);
+  uint32_t phase = 0;
+#ifdef VK_FACTOR_TRACE
+  long long trc[4] = {0, 0, 0, 0}, tt0 = clock64();
+#endif
+
+  for (int bb = blockIdx.x; bb < count; bb += gridDim.x) {
+    const int p = plist[bb];
+    const int s = static_cast<int>(off[p + 1] - off[p]);
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    double a[C];
+    double m = 0.0;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int c = ch * C + j;
+      a[j] = (i < s && c < s) ? stage[blk_at(i, c, s)] : 0.0;
+      m = fmax(m, fabs(a[j]));
+    }
+    rsh[ch][i] = m;
+    if (t == 0) s_bad = 0;
+    __syncthreads();                                  // stage consumed: prefetch the next block
+    if (t == 0 && bb + static_cast<int>(gridDim.x) < count)
+      stage_block(plist[bb + gridDim.x], off, opoff, inv, stage, &bar, pol);
+    double rsc = rsh[0][i];
+#pragma unroll
+    for (int c = 1; c < CH; ++c) rsc = fmax(rsc, rsh[c][i]);
+    if (ch == 0 && i < s && rsc == 0.0) s_bad = VK_PATCH_ZERO_ROW;   // sparsela.py:74-77
+    __syncthreads();
+    VK_TRACE_ADD(0, tt0);
+#ifdef VK_FACTOR_TRACE
+    tt0 = clock64();
+#endif
+    if (s_bad) {
+      if (t == 0) status[p] = s_bad;
+      continue;
+    }
+    int pos = (i < s) ? i : NONE;                     // LAPACK position of this row
+
+    // candidate of this row-warp for step k (warps holding column k): first
+    // maximum |a_ik| over the open positions, published with |value|,
+    // position, row and guard verdict (and, for two column halves, its row
+    // scaled by its own reciprocal: the other half waits only for the winner)
+    auto candidate = [&](int k) {
+      const int b = k & 1;
+      const double f = a[0];
+      if (CH > 1) fcol[b][i] = f;
+      const bool open = pos >= k && pos < s;
+      const unsigned long long key =
+          open ? static_cast<unsigned long long>(__double_as_longlong(fabs(f))) : 0ull;
+      const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+      const unsigned mhi = __reduce_max_sync(FULL, hi);
+      unsigned eq = __ballot_sync(FULL, open && hi == mhi);
+      if (__popc(eq) > 1) {                             // tie on the high word (rare)
+        const unsigned mlo = __reduce_max_sync(FULL, (eq >> lane) & 1u ? lo : 0u);
+        eq = __ballot_sync(FULL, ((eq >> lane) & 1u) && lo == mlo);
+        if (__popc(eq) > 1) {                           // exact tie: lowest position
+          const unsigned pm = __reduce_min_sync(
+              FULL, (eq >> lane) & 1u ? static_cast<unsigned>(pos) : 0x7fffffffu);
+          eq = __ballot_sync(FULL, ((eq >> lane) & 1u) && static_cast<unsigned>(pos) == pm);
+        }
+      }
+      if (eq == 0u) {
+        if (lane == 0) cpos[b][wr] = NONE;
+      } else if (lane == __ffs(eq) - 1) {
+        if (CH > 1) {
+          const double rc = __drcp_rn(f);               // == 1.0 / f (correctly rounded)
+          double* dst = cb[b][wr];
+          dst[0] = rc;
+#pragma unroll
+          for (int j = 1; j < C; ++j) dst[j] = a[j] * rc;
+        }
+        cabs[b][wr] = fabs(f);
+        cpos[b][wr] = pos;
+        crow[b][wr] = i;
+        cok[b][wr] = fabs(f) >= 1e-12 * rsc;            // sparsela.py:79-83
+      }
+    };
+
+    int bad = 0;
+    if (ch == 0) candidate(0);
+    for (int k = 0; k < s; ++k) {
+      const int b = k & 1;
+      const bool own = (CH == 1) || ch == k / C;        // warp-uniform
+      __syncthreads();
+      // the same winner in every warp: largest |value|, lowest position on ties
+      int bw = 0;
+      if (NWR > 1) {
+        double best = -1.0;
+        int bp = NONE;
+#pragma unroll
+        for (int w = 0; w < NWR; ++w) {
+          const int ps = cpos[b][w];
+          const double av = cabs[b][w];
+          if (ps != NONE && (av > best || (av == best && ps < bp))) {
+            best = av;
+            bp = ps;
+            bw = w;
+          }
+        }
+      }
+      if (!cok[b][bw]) {                                // block-uniform
+        bad = VK_PATCH_SMALL_PIVOT;
+        break;
+      }
+      const int ppos = cpos[b][bw], r = crow[b][bw];
+      const bool isp = (i == r);
+      const double* P = cb[b][bw];
+      double rinv;
+      if (CH == 1) {                                    // the winner scales and publishes
+        if (isp) {                                      // (one lane; its registers become
+          rinv = __drcp_rn(a[0]);                       //  the scaled row)
+          double2* P2w = reinterpret_cast<double2*>(cb[b][0]);
+#pragma unroll
+          for (int jj = 0; jj < C / 2; ++jj) {
+            const double x = (jj == 0) ? rinv : a[2 * jj] * rinv;
+            const double y = a[2 * jj + 1] * rinv;
+            if (jj > 0) a[2 * jj] = x;
+            a[2 * jj + 1] = y;
+            P2w[jj] = make_double2(x, y);
+          }
+        }
+        __syncthreads();
+        P = cb[b][0];
+        rinv = P[0];
+      } else {
+        rinv = P[0];
+      }
+      if (own) {
+        const double f = a[0];
+        if (CH > 1 && isp) {                            // its registers become the scaled row
+#pragma unroll
+          for (int j = 1; j < C; ++j) a[j] *= rinv;
+        }
+        const double g = isp ? 0.0 : f;                 // fma(-0, p, a) == a exactly
+        const double2* P2 = reinterpret_cast<const double2*>(P);
+        // rotate: register j-1 <- column j
+#pragma unroll
+        for (int jj = 0; jj < C / 2; ++jj) {
+          const double2 q = P2[jj];
+          if (jj > 0) a[2 * jj - 1] = fma(-g, q.x, a[2 * jj]);
+          a[2 * jj] = fma(-g, q.y, a[2 * jj + 1]);
+        }
+        a[C - 1] = isp ? rinv : -f * rinv;
+      } else {
+        const double f = fcol[b][i];
+        if (isp) {                                      // the pivot row, this column group
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            a[j] *= rinv;
+            ob[ch * C + j] = a[j];
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * NWR * (CH - 1)) : "memory");   // other groups
+        const double g = isp ? 0.0 : f;
+        const double2* P2 = reinterpret_cast<const double2*>(ob + ch * C);
+#pragma unroll
+        for (int jj = 0; jj < C / 2; ++jj) {
+          const double2 q = P2[jj];
+          a[2 * jj] = fma(-g, q.x, a[2 * jj]);
+          a[2 * jj + 1] = fma(-g, q.y, a[2 * jj + 1]);
+        }
+      }
+      pos = isp ? k : ((pos == k) ? ppos : pos);
+      if (k + 1 < s && ((CH == 1) || ch == (k + 1) / C)) candidate(k + 1);
+    }
+    VK_TRACE_ADD(1, tt0);
+#ifdef VK_FACTOR_TRACE
+    tt0 = clock64();
+#endif
+    if (bad) {
+      if (t == 0) status[p] = bad;
+      continue;
+    }
+    if (ch == 0 && i < s) perm[pos] = i;
+    __syncthreads();
+    // Ainv[x][y] = W[perm x][posof y]: row i (position pos), column c goes
+    // to column-major dst[perm[c] s + pos]
+    if (i < s) {
+      double* dst = inv + opoff[p];
+      const int n = min(max(s - ch * C, 0), C);         // rotations of this half
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        int c = j + n;
+        c = (c >= C ? c - C : c) + ch * C;
+        if (c < s) dst[perm[c] * s + pos] = a[j];
+      }
+    }
+    if (t == 0) status[p] = VK_PATCH_OK;
+    __syncthreads();                                  // perm reuse
+    VK_TRACE_ADD(2, tt0);
+#ifdef VK_FACTOR_TRACE
+    tt0 = clock64();
+#endif
+  }
+#ifdef VK_FACTOR_TRACE
+  if (blockIdx.x == 0 && t == 0)
+    printf("[rows C=%d NWR=%d CH=%d] load %lld steps %lld output %lld (cycles, %d patches)\n",
+           C, NWR, CH, trc[0], trc[1], trc[2], (count + gridDim.x - 1) / gridDim.x);
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// One warp per patch (K3 for s <= 48): R block rows per lane (i = lane + 32q),
+// all C columns in registers, rotated like factor_rows_kernel.  No CTA
+// barriers: the pivot search is a warp vote, the winner lane scales its row in
+// registers and publishes it through a per-warp double buffer, one __syncwarp
+// per step.  Same pivots, guard and per-element arithmetic as the other K3
+// kernels (bit-identical inverses).  Blocks arrive by bulk copy (staged by
+// extract_blocks_kernel), the next one while this one is factored.
+template <int C, int R, int MB>
+__global__ void __launch_bounds__(32, MB) factor_warp_kernel(
+    const int* __restrict__ plist, int count, const int64_t* __restrict__ off,
+    const int64_t* __restrict__ opoff, double* __restrict__ inv, int* __restrict__ status) {
+  constexpr int S = C;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int NONE = 0x7fffffff;
+  static_assert(C % 2 == 0 && 32 * R >= S, "rows per lane / column pairs");
+  extern __shared__ __align__(16) double stage[];     // the staged block (blk_at layout)
+  __shared__ __align__(16) double prow[2][C];         // scaled pivot row (rotated frame)
+  __shared__ int perm[S];
+  __shared__ __align__(8) uint64_t bar;
+  const int lane = threadIdx.x;
+  const uint64_t pol = evict_first_policy();
+  if (lane == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  if (lane == 0 && static_cast<int>(blockIdx.x) < count)
+    stage_block(plist[blockIdx.x], off, opoff, inv, stage, &bar, pol);
+  uint32_t phase = 0;
+#ifdef VK_FACTOR_TRACE
+  long long trc[4] = {0, 0, 0, 0}, tt0 = clock64();
+#endif
+
+  for (int bb = blockIdx.x; bb < count; bb += gridDim.x) {
+    const int p = plist[bb];
+    const int s = static_cast<int>(off[p + 1] - off[p]);
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    double a[R][C], rsc[R];
+    int pos[R];
+    bool zero = false;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = lane + 32 * q;
+      double m = 0.0;
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        a[q][j] = (i < s && j < s) ? stage[blk_at(i, j, s)] : 0.0;
+        m = fmax(m, fabs(a[q][j]));
+      }
+      rsc[q] = m;
+      pos[q] = (i < s) ? i : NONE;
+      zero |= (i < s && m == 0.0);
+    }
+    __syncwarp();                                      // stage consumed: prefetch the next block
+    if (lane == 0 && bb + static_cast<int>(gridDim.x) < count)
+      stage_block(plist[bb + gridDim.x], off, opoff, inv, stage, &bar, pol);
+    VK_TRACE_ADD(0, tt0);
+#ifdef VK_FACTOR_TRACE
+    tt0 = clock64();
+#endif
+    if (__any_sync(FULL, zero)) {                      // sparsela.py:74-77
+      if (lane == 0) status[p] = VK_PATCH_ZERO_ROW;
+      continue;
+    }
+    int bad = 0;
+    for (int k = 0; k < s; ++k) {
+      const int b = k & 1;
+      // this lane's best open row: largest |a_i,k|, lowest position on ties
+      unsigned long long bkey = 0ull;
+      int bpos = NONE, bq = 0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const unsigned long long key =
+            static_cast<unsigned long long>(__double_as_longlong(fabs(a[q][0])));
+        const bool open = pos[q] >= k && pos[q] < s;
+        if (open && (bpos == NONE || key > bkey || (key == bkey && pos[q] < bpos))) {
+          bkey = key;
+          bpos = pos[q];
+          bq = q;
+        }
+      }
+      const bool any = bpos != NONE;
+      const unsigned hi = static_cast<unsigned>(bkey >> 32), lo = static_cast<unsigned>(bkey);
+      const unsigned mhi = __reduce_max_sync(FULL, any ? hi : 0u);
+      unsigned eq = __ballot_sync(FULL, any && hi == mhi);
+      if (__popc(eq) > 1) {                            // tie on the high word (rare)
+        const unsigned mlo = __reduce_max_sync(FULL, (eq >> lane) & 1u ? lo : 0u);
+        eq = __ballot_sync(FULL, ((eq >> lane) & 1u) && lo == mlo);
+        if (__popc(eq) > 1) {                          // exact tie: lowest position
+          const unsigned pm = __reduce_min_sync(
+              FULL, (eq >> lane) & 1u ? static_cast<unsigned>(bpos) : 0x7fffffffu);
+          eq = __ballot_sync(FULL, ((eq >> lane) & 1u) && static_cast<unsigned>(bpos) == pm);
+        }
+      }
+      const int wl = __ffs(eq) - 1;
+      const int ppos = __shfl_sync(FULL, bpos, wl);
+      const int qw = __shfl_sync(FULL, bq, wl);
+      int ok = 1;
+      if (lane == wl) {                                // scale and publish the pivot row
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          if (q != qw) continue;
+          const double f = a[q][0];
+          ok = fabs(f) >= 1e-12 * rsc[q];              // sparsela.py:79-83
+          const double rinv = __drcp_rn(f);            // == 1.0 / f (correctly rounded)
+          double2* P2w = reinterpret_cast<double2*>(prow[b]);
+#pragma unroll
+          for (int jj = 0; jj < C / 2; ++jj) {
+            const double x = (jj == 0) ? rinv : a[q][2 * jj] * rinv;
+            const double y = a[q][2 * jj + 1] * rinv;
+            if (jj > 0) a[q][2 * jj] = x;
+            a[q][2 * jj + 1] = y;
+            P2w[jj] = make_double2(x, y);
+          }
+        }
+      }
+      if (!__shfl_sync(FULL, ok, wl)) {                // warp-uniform
+        bad = VK_PATCH_SMALL_PIVOT;
+        break;
+      }
+      __syncwarp();
+      const double2* P2 = reinterpret_cast<const double2*>(prow[b]);
+      double g[R], fq[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        fq[q] = a[q][0];
+        g[q] = (lane == wl && q == qw) ? 0.0 : fq[q];  // fma(-0, p, a) == a exactly
+      }
+      double rinv = 0.0;
+      // rotate: register j-1 <- column j
+#pragma unroll
+      for (int jj = 0; jj < C / 2; ++jj) {
+        const double2 pq = P2[jj];
+        if (jj == 0) rinv = pq.x;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          if (jj > 0) a[q][2 * jj - 1] = fma(-g[q], pq.x, a[q][2 * jj]);
+          a[q][2 * jj] = fma(-g[q], pq.y, a[q][2 * jj + 1]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const bool isp = (lane == wl && q == qw);
+        a[q][C - 1] = isp ? rinv : -fq[q] * rinv;
+        pos[q] = isp ? k : ((pos[q] == k) ? ppos : pos[q]);
+      }
+    }
+    VK_TRACE_ADD(1, tt0);
+#ifdef VK_FACTOR_TRACE
+    tt0 = clock64();
+#endif
+    if (bad) {
+      if (lane == 0) status[p] = bad;
+      continue;
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (lane + 32 * q < s) perm[pos[q]] = lane + 32 * q;
+    __syncwarp();
+    // row i (position pos), column c -> column-major dst[perm[c] s + pos]
+    // (s rotations: register j holds column (j + s) mod C)
+    double* dst = inv + opoff[p];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      if (lane + 32 * q < s) {
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+          int c = j + s;
+          c = c >= C ? c - C : c;
+          if (c < s) dst[perm[c] * s + pos[q]] = a[q][j];
+        }
+      }
+    }
+    if (lane == 0) status[p] = VK_PATCH_OK;
+    __syncwarp();                                      // perm reuse
+    VK_TRACE_ADD(2, tt0);
+#ifdef VK_FACTOR_TRACE
+    tt0 = clock64();
+#endif
+  }
+#ifdef VK_FACTOR_TRACE
+  if (blockIdx.x == 0 && lane == 0)
+    printf("[warp C=%d R=%d] load %lld steps %lld output %lld (cycles, %d patches)\n", C, R,
+           trc[0], trc[1], trc[2], (count + gridDim.x - 1) / gridDim.x);
+#endif
+}
+
+template <int C, int R, int MB>
+cudaError_t launch_warp(const int* d_ids, int count, const vk_patches_s* h, int* d_status,
+                        cudaStream_t st) {
+  auto kern = factor_warp_kernel<C, R, MB>;
+  const size_t dsm = sizeof(double) * size_t((C * C + 1) & ~1);
+  cudaError_t e = vk_smem_optin((const void*)kern, int(dsm));
+  if (e != cudaSuccess) return e;
+  const int grid = std::max(1, std::min(count, vk_resident_blocks((const void*)kern, 32, dsm)));
+  kern<<<grid, 32, dsm, st>>>(d_ids, count, h->off, h->opoff, h->inv, d_status);
+  return cudaGetLastError();
+}
+
+// VK_FACTOR_ROWS=0 keeps the round-2 kernels (register tiles / DMMA)
+bool rows_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("VK_FACTOR_ROWS");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// largest patch size factored by the staged kernels (rows / warp); the
+// classes above run the DMMA kernel (VK_FACTOR_ROWS_MAX overrides, <= 128)
+int rows_max() {
+  static const int v = [] {
+    const char* e = getenv("VK_FACTOR_ROWS_MAX");
+    return e ? std::max(0, std::min(kXCols, atoi(e))) : 96;
+  }();
+  return rows_enabled() ? v : 0;
+}
+
+template <int C, int NWR, int CH, int MB>
+cudaError_t launch_rows(const int* d_ids, int count, const vk_patches_s* h, int* d_status,
+                        cudaStream_t st) {
+  auto kern = factor_rows_kernel<C, NWR, CH, MB>;
+  constexpr int NT = 32 * NWR * CH;
+  const size_t dsm = sizeof(double) * size_t((C * CH * C * CH + 1) & ~1);
+  cudaError_t e = vk_smem_optin((const void*)kern, int(dsm));
+  if (e != cudaSuccess) return e;
+  const int grid = std::max(1, std::min(count, vk_resident_blocks((const void*)kern, NT, dsm)));
+  kern<<<grid, NT, dsm, st>>>(d_ids, count, h->off, h->opoff, h->inv, d_status);
+  return cudaGetLastError();
+}
+
 // One size class: d_ids (device) lists its patches.  Asynchronous on st.
 int launch_class(int smax, const int* d_ids, int count, const vk_patches_s* h, const vk::Csr* a,
                  int* d_status, double* blocks, const int64_t* d_boff, int extract_only,
                  cudaStream_t st) {
   if (count == 0) return VK_OK;
   const size_t smem = factor_smem_bytes(smax);
+  if (!extract_only && smax <= rows_max()) {
+    cudaError_t e;
+    if (smax <= 16) e = launch_warp<16, 1, 24>(d_ids, count, h, d_status, st);
+    else if (smax <= 24) e = launch_warp<24, 1, 20>(d_ids, count, h, d_status, st);
+    else if (smax <= 32) e = launch_warp<32, 1, 16>(d_ids, count, h, d_status, st);
+    else if (smax <= 40) e = launch_warp<40, 2, 8>(d_ids, count, h, d_status, st);
+    else if (smax <= 48) e = launch_warp<48, 2, 8>(d_ids, count, h, d_status, st);
+    else if (smax <= 56) e = launch_rows<56, 2, 1, 6>(d_ids, count, h, d_status, st);
+    else if (smax <= 64) e = launch_rows<64, 2, 1, 5>(d_ids, count, h, d_status, st);
+    else if (smax <= 80) e = launch_rows<40, 3, 2, 2>(d_ids, count, h, d_status, st);
+    else if (smax <= 96) e = launch_rows<48, 3, 2, 2>(d_ids, count, h, d_status, st);
+    else if (smax <= 104) e = launch_rows<26, 4, 4, 1>(d_ids, count, h, d_status, st);
+    else if (smax <= 112) e = launch_rows<28, 4, 4, 1>(d_ids, count, h, d_status, st);
+    else e = launch_rows<32, 4, 4, 1>(d_ids, count, h, d_status, st);
+    if (e != cudaSuccess) {
+      vk::set_error("factor_rows_kernel: %s", cudaGetErrorString(e));
+      return VK_ERR_CUDA;
+    }
+    return VK_OK;
+  }
   if (!extract_only && smax > 64 && smax <= 128 && dmma_enabled()) {
     cudaError_t e = cudaSuccess;
 #define VK_DMMA(S_)                                                                             \
@@ -1117,6 +1726,57 @@ int launch_bucket_sync(const Bucket& bk, const vk_patches_s* h, const vk::Csr* a
   return st;
 }
 
+std::mutex g_factor_mutex;   // factorisations / extractions (shared streams, handle maps)
+
+// extraction map for matrix a (built by the first factorisation against it,
+// kept in the handle): for every patch row and stored CSR entry of that row,
+// the local column in the patch (-1 if absent) -- later extractions gather
+// without searching
+int ensure_emap(vk_patches_s* h, const vk::Csr* a) {
+  if (h->fac_emap_key != a->uid && h->npatch > 0) {
+    cudaFree(h->fac_emap);
+    h->fac_emap = nullptr;
+    h->fac_emap_key = 0;
+    if (!h->fac_eoff) VK_CHECK_CUDA(cudaMalloc(&h->fac_eoff, sizeof(int64_t) * (h->total + 1)));
+    VK_CHECK_CUDA(cudaMemset(h->fac_eoff, 0, sizeof(int64_t) * (h->total + 1)));
+    entry_count_kernel<<<vk_grid(h->total, 256), 256>>>(h->total, h->idx, a->indptr, h->fac_eoff);
+    VK_CHECK_LAUNCH();
+    size_t tb = 0;
+    VK_CHECK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, h->fac_eoff, h->fac_eoff,
+                                                h->total + 1));
+    void* tmp = nullptr;
+    VK_CHECK_CUDA(cudaMalloc(&tmp, std::max<size_t>(tb, 1)));
+    cudaError_t se = cub::DeviceScan::InclusiveSum(tmp, tb, h->fac_eoff, h->fac_eoff,
+                                                   h->total + 1);
+    cudaFree(tmp);
+    VK_CHECK_CUDA(se);
+    int64_t etotal = 0;
+    VK_CHECK_CUDA(cudaMemcpy(&etotal, h->fac_eoff + h->total, sizeof(int64_t),
+                             cudaMemcpyDeviceToHost));
+    VK_CHECK_CUDA(cudaMalloc(&h->fac_emap, sizeof(int16_t) * std::max<int64_t>(etotal, 1)));
+    emap_fill_kernel<<<vk_grid(int64_t(h->npatch) * 32, 128, 148 * 16), 128>>>(
+        h->npatch, h->off, h->idx, a->indptr, a->indices, h->fac_eoff, h->fac_emap);
+    VK_CHECK_LAUNCH();
+    h->fac_emap_key = a->uid;
+  }
+  return VK_OK;
+}
+
+// K2 for every patch of [p0, p1) with s <= kXCols into out (slot offsets
+// opoff - obase), staged layout blk_at; stream st
+int launch_extract(vk_patches_s* h, const vk::Csr* a, int p0, int p1, int scut,
+                   const int64_t* opoff, int64_t obase, double* out, cudaStream_t st) {
+  if (p1 <= p0) return VK_OK;
+  const size_t xs = sizeof(double) * size_t(8 * kXRows * kXCols);
+  VK_CHECK_CUDA(vk_smem_optin((const void*)extract_blocks_kernel, int(xs)));
+  const int grid = std::max(1, std::min((p1 - p0 + 7) / 8,
+                                        vk_resident_blocks((const void*)extract_blocks_kernel, 256, xs)));
+  extract_blocks_kernel<<<grid, 256, xs, st>>>(p0, p1, std::min(scut, kXCols), h->off, h->idx, a->indptr, a->data,
+                                               h->fac_eoff, h->fac_emap, opoff, obase, out);
+  VK_CHECK_LAUNCH();
+  return VK_OK;
+}
+
 }  // namespace
 
 extern "C" int vk_extract(vk_csr_t a, const int32_t* rows, int32_t nrows, const int32_t* cols,
@@ -1137,32 +1797,62 @@ extern "C" int vk_patches_extract(vk_patches_t h, vk_csr_t a, int32_t first, int
              a->nrows, a->ncols, h->ndof);
   if (count == 0) return VK_OK;
   VK_REQUIRE(h->smax <= kMaxPatch, "patch size %d exceeds %d", h->smax, kMaxPatch);
-  auto buckets = make_buckets(h->h_off, first, count);
-  // block offsets in patch order
-  std::vector<int64_t> rel(count + 1, 0);
+  std::lock_guard<std::mutex> lock(g_factor_mutex);   // the extraction map lives in the handle
+  // blocks of up to kXCols rows: the production K2 pass (extract_blocks_kernel,
+  // staged layout) into a scratch laid out like the operator slots; larger
+  // blocks: the shared-memory kernel's extraction (row-major)
+  std::vector<int64_t> rel(count + 1, 0), oo(h->npatch + 1, 0);
   for (int q = 0; q < count; ++q) {
     const int64_t s = h->h_off[first + q + 1] - h->h_off[first + q];
     rel[q + 1] = rel[q] + s * s;
+    oo[first + q + 1] = oo[first + q] + ((s * s + 1) & ~int64_t(1));
+  }
+  for (int p = first + count + 1; p <= h->npatch; ++p) oo[p] = oo[first + count];
+  {
+    const int est = ensure_emap(h, a);
+    if (est) return est;
   }
   double* d_blocks = nullptr;
+  double* d_stage = nullptr;
+  int64_t* d_oo = nullptr;
   int* d_status = nullptr;
   VK_CHECK_CUDA(cudaMalloc(&d_blocks, sizeof(double) * std::max<int64_t>(rel[count], 1)));
+  VK_CHECK_CUDA(cudaMalloc(&d_stage, sizeof(double) * std::max<int64_t>(oo[h->npatch], 2)));
+  VK_CHECK_CUDA(cudaMalloc(&d_oo, sizeof(int64_t) * (h->npatch + 1)));
   VK_CHECK_CUDA(cudaMalloc(&d_status, sizeof(int) * h->npatch));
-  int st = VK_OK;
+  VK_CHECK_CUDA(cudaMemcpy(d_oo, oo.data(), sizeof(int64_t) * (h->npatch + 1), cudaMemcpyHostToDevice));
+  int st = launch_extract(h, a, first, first + count, kXCols, d_oo, 0, d_stage, 0);
+  auto buckets = make_buckets(h->h_off, first, count);
   for (auto& bk : buckets) {
+    if (st || bk.smax <= kXCols) continue;
     std::vector<int64_t> boff(bk.ids.size());
     for (size_t q = 0; q < bk.ids.size(); ++q) boff[q] = rel[bk.ids[q] - first];
     st = launch_bucket_sync(bk, h, a, d_status, d_blocks, boff);
-    if (st) break;
   }
+  std::vector<double> staged(oo[h->npatch]);
   if (!st) {
-    cudaError_t e = cudaMemcpy(blocks_host, d_blocks, sizeof(double) * rel[count], cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess)
+      e = cudaMemcpy(blocks_host, d_blocks, sizeof(double) * rel[count], cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(staged.data(), d_stage, sizeof(double) * oo[h->npatch], cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) {
       vk::set_error("vk_patches_extract: %s", cudaGetErrorString(e));
       st = VK_ERR_CUDA;
     }
   }
+  if (!st)
+    for (int q = 0; q < count; ++q) {                 // un-stage into row-major blocks
+      const int s = static_cast<int>(h->h_off[first + q + 1] - h->h_off[first + q]);
+      if (s > kXCols) continue;
+      const double* src = staged.data() + oo[first + q];
+      double* dst = blocks_host + rel[q];
+      for (int i = 0; i < s; ++i)
+        for (int j = 0; j < s; ++j) dst[i * s + j] = src[blk_at(i, j, s)];
+    }
   cudaFree(d_blocks);
+  cudaFree(d_stage);
+  cudaFree(d_oo);
   cudaFree(d_status);
   return st;
 }
@@ -1171,8 +1861,7 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
   VK_REQUIRE(h && a, "vk_patches_factor: null argument");
   // setup-time call: serialised, because the auxiliary stream and its
   // fork/join events below are shared by all handles
-  static std::mutex factor_mutex;
-  std::lock_guard<std::mutex> lock(factor_mutex);
+  std::lock_guard<std::mutex> lock(g_factor_mutex);
   VK_REQUIRE(a->nrows == h->ndof && a->ncols == h->ndof,
              "vk_patches_factor: matrix is %dx%d, patches need %d", a->nrows, a->ncols, h->ndof);
   if (h->smax > kMaxPatch) {
@@ -1217,34 +1906,31 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
     VK_CHECK_CUDA(cudaMalloc(&h->fac_status, sizeof(int32_t) * std::max(h->npatch, 1)));
   }
   int* d_status = h->fac_status;
-  // extraction map for this matrix (first factorisation against it): later
-  // factorisations gather the block entries without searching
-  if (h->fac_emap_key != a->uid && h->npatch > 0) {
-    cudaFree(h->fac_emap);
-    h->fac_emap = nullptr;
-    h->fac_emap_key = 0;
-    if (!h->fac_eoff) VK_CHECK_CUDA(cudaMalloc(&h->fac_eoff, sizeof(int64_t) * (h->npatch + 1)));
-    VK_CHECK_CUDA(cudaMemset(h->fac_eoff, 0, sizeof(int64_t) * (h->npatch + 1)));
-    entry_count_kernel<<<vk_grid(h->npatch, 256), 256>>>(h->npatch, h->off, h->idx, a->indptr,
-                                                        h->fac_eoff);
-    VK_CHECK_LAUNCH();
-    size_t tb = 0;
-    VK_CHECK_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, h->fac_eoff, h->fac_eoff,
-                                                h->npatch + 1));
-    void* tmp = nullptr;
-    VK_CHECK_CUDA(cudaMalloc(&tmp, std::max<size_t>(tb, 1)));
-    cudaError_t se = cub::DeviceScan::InclusiveSum(tmp, tb, h->fac_eoff, h->fac_eoff,
-                                                   h->npatch + 1);
-    cudaFree(tmp);
-    VK_CHECK_CUDA(se);
-    int64_t etotal = 0;
-    VK_CHECK_CUDA(cudaMemcpy(&etotal, h->fac_eoff + h->npatch, sizeof(int64_t),
-                             cudaMemcpyDeviceToHost));
-    VK_CHECK_CUDA(cudaMalloc(&h->fac_emap, sizeof(int16_t) * std::max<int64_t>(etotal, 1)));
-    emap_fill_kernel<<<vk_grid(int64_t(h->npatch) * 32, 128, 148 * 16), 128>>>(
-        h->npatch, h->off, h->idx, a->indptr, a->indices, h->fac_eoff, h->fac_emap);
-    VK_CHECK_LAUNCH();
-    h->fac_emap_key = a->uid;
+  {
+    const int est = ensure_emap(h, a);
+    if (est) return est;
+  }
+  // K2: every block of the staged classes into its operator slot (the staged
+  // K3 kernels stream them from there)
+  if (rows_max() > 0) {
+    static const bool timing_x = getenv("VK_FACTOR_TIMING") != nullptr;
+    cudaEvent_t x0 = nullptr, x1 = nullptr;
+    if (timing_x) {
+      cudaEventCreate(&x0);
+      cudaEventCreate(&x1);
+      cudaEventRecord(x0, 0);
+    }
+    const int xst = launch_extract(h, a, 0, h->npatch, rows_max(), h->opoff, 0, h->inv, 0);
+    if (xst) return xst;
+    if (timing_x) {
+      cudaEventRecord(x1, 0);
+      cudaEventSynchronize(x1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, x0, x1);
+      fprintf(stderr, "[vk_factor] extraction (K2): %d patches, %.3f ms\n", h->npatch, ms);
+      cudaEventDestroy(x0);
+      cudaEventDestroy(x1);
+    }
   }
   // The largest class (most work) runs on the legacy stream, the small ones
   // (boundary / coarse patches) beside it on an auxiliary stream; one join.
