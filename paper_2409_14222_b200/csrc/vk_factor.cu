@@ -59,6 +59,16 @@ __device__ __forceinline__ void warp_scan_rows(int lane, int s, int* rowoff) {
   if (lane == 0) rowoff[0] = 0;
 }
 
+// position of A[i][j] in a staged block (see extract_blocks_kernel)
+__host__ __device__ __forceinline__ int blk_at(int i, int j, int s) {
+  int c = j;
+  if (!(s & 1)) {
+    c = j + i;
+    if (c >= s) c -= s;
+  }
+  return i * s + c;
+}
+
 // Extraction of the dense patch block A[idx, idx] from the CSR with every
 // (row, stored entry) pair as an independent work item: thread t takes
 // entries t, t + nth, ..., four in flight, finds its row by binary search in
@@ -738,6 +748,386 @@ __global__ void __launch_bounds__(256, (S <= 96) ? 2 : 1) factor_dmma_kernel(
 #endif
 }
 
+// ---------------------------------------------------------------------------
+// Blocked Gauss-Jordan with FP64 DMMA updates for the large classes
+// (96 < s <= 128 by default), round-3 form of factor_dmma_kernel:
+//   * the block arrives from the K2 pass (staged slot, coalesced loads; the
+//     next patch's slot is prefetched into L2 while this one is factored);
+//   * panel factorisation (warp 0, registers, rows lane + 32q): per column a
+//     redux.sync on the high word of |a| plus a ballot (ties resolved exactly,
+//     lowest position first), the winner lane scales its row in registers and
+//     publishes it through shared memory; row scales live in registers; no
+//     select chains over the panel;
+//   * look-ahead: warps 1..7 update panel p+1's column tile first, a named
+//     barrier hands it to warp 0, which factors panel p+1 while warps 1..7
+//     apply panel p to the rest of the block (8x8 DMMA tiles,
+//     C = (pivot row ? 0 : C) + Pn R as in factor_dmma_kernel).
+template <int S, int R>
+__device__ __forceinline__ int factor_panel2(double* W, double* Pb, int (&pos)[R],
+                                             const double (&rsc)[R], int* isp, int* pids,
+                                             double* pbuf, int k0, int lane) {
+  constexpr int LD = S + 1, NB = 8;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int NONE = 0x7fffffff;
+  double pan[R][NB];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int r = lane + 32 * q;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) pan[q][c] = (r < S) ? W[r * LD + k0 + c] : 0.0;
+  }
+  int okall = 1;
+#pragma unroll
+  for (int kk = 0; kk < NB; ++kk) {
+    const int k = k0 + kk;
+    // this lane's best open row (branch-free): largest |a|, lowest position
+    double bv = -1.0;
+    int bpos = NONE, bq = 0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const double v = fabs(pan[q][kk]);
+      const bool open = pos[q] >= k && pos[q] < S;
+      const bool better = open && (v > bv || (v == bv && pos[q] < bpos));
+      bv = better ? v : bv;
+      bpos = better ? pos[q] : bpos;
+      bq = better ? q : bq;
+    }
+    const bool any = bpos != NONE;
+    const unsigned long long key =
+        any ? static_cast<unsigned long long>(__double_as_longlong(bv)) : 0ull;
+    const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+    const unsigned mhi = __reduce_max_sync(FULL, hi);
+    unsigned eq = __ballot_sync(FULL, any && hi == mhi);
+    if (__popc(eq) > 1) {
+      const unsigned mlo = __reduce_max_sync(FULL, (eq >> lane) & 1u ? lo : 0u);
+      eq = __ballot_sync(FULL, ((eq >> lane) & 1u) && lo == mlo);
+      if (__popc(eq) > 1) {
+        const unsigned pm = __reduce_min_sync(
+            FULL, (eq >> lane) & 1u ? static_cast<unsigned>(bpos) : 0x7fffffffu);
+        eq = __ballot_sync(FULL, ((eq >> lane) & 1u) && static_cast<unsigned>(bpos) == pm);
+      }
+    }
+    const int wl = __ffs(eq) - 1;
+    // the winner publishes its raw panel row, position, slot and guard verdict;
+    // every lane forms 1/pivot and the scaled row itself (same operations as
+    // the unblocked kernels, so the values are identical)
+    double* pb = pbuf + (kk & 1) * (NB + 2);
+    if (lane == wl) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q != bq) continue;
+#pragma unroll
+        for (int c = 0; c < NB; c += 2)
+          *reinterpret_cast<double2*>(pb + c) = make_double2(pan[q][c], pan[q][c + 1]);
+        const int ok = fabs(pan[q][kk]) >= 1e-12 * rsc[q];   // sparsela.py:79-83
+        reinterpret_cast<int*>(pb + NB)[0] = bpos;
+        reinterpret_cast<int*>(pb + NB)[1] = q;
+        reinterpret_cast<int*>(pb + NB + 1)[0] = ok;
+      }
+    }
+    __syncwarp();
+    double prow[NB];
+#pragma unroll
+    for (int c = 0; c < NB; c += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(pb + c);
+      prow[c] = v.x;
+      prow[c + 1] = v.y;
+    }
+    const int ppos = reinterpret_cast<const int*>(pb + NB)[0];
+    const int qw = reinterpret_cast<const int*>(pb + NB)[1];
+    okall &= reinterpret_cast<const int*>(pb + NB + 1)[0];
+    const double rinv = __drcp_rn(prow[kk]);           // == 1.0 / pivot (correctly rounded)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) prow[c] = (c == kk) ? rinv : prow[c] * rinv;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const double f = pan[q][kk];
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        pan[q][c] = (c == kk) ? -f * rinv : fma(-f, prow[c], pan[q][c]);
+    }
+    if (lane == wl) {                                  // the pivot row: the scaled row
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (q == qw) {
+#pragma unroll
+          for (int c = 0; c < NB; ++c) pan[q][c] = prow[c];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const bool isp = (lane == wl && q == qw);
+      pos[q] = isp ? k : ((pos[q] == k) ? ppos : pos[q]);
+    }
+    if (lane == 0) pids[kk] = wl + 32 * qw;
+  }
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int r = lane + 32 * q;
+    if (r < S) {
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        W[r * LD + k0 + c] = pan[q][c];
+        Pb[r * NB + c] = pan[q][c];
+      }
+    }
+  }
+  __syncwarp();
+  if (!okall) return VK_PATCH_SMALL_PIVOT;
+  if (lane < NB) isp[pids[lane]] = 1;
+  return VK_PATCH_OK;
+}
+
+// warps 1..7 of factor_blk_kernel: the rank-8 Gauss-Jordan update of the
+// block by panel pp (C = (pivot row ? 0 : C) + Pn R on 8x8 DMMA tiles) for
+// every column tile except pp (already final) and pp+1 when `skip1` (done
+// first by the look-ahead).  Work units are (tile row, half of the column
+// tiles), dealt round-robin to the 7 warps; the A fragments and pivot-row
+// flags of a tile row are loaded once per unit, four tiles are in flight.
+template <int S>
+__device__ __forceinline__ void blk_update(double* W, const double* Pb, const double* Rb,
+                                           const int* isp, int pp, bool skip1, int w, int nw,
+                                           int lane) {
+  constexpr int LD = S + 1, TT = S / 8, H0 = (TT + 1) / 2;
+  const int g = lane >> 2, m = lane & 3;
+  for (int u = w; u < 2 * TT; u += nw) {
+    const int ti = u >> 1, half = u & 1;
+    const int t0 = half ? H0 : 0, t1 = half ? TT : H0;
+    const int row = ti * 8 + g;
+    const double a0 = Pb[row * 8 + m], a1 = Pb[row * 8 + 4 + m];
+    const bool zr = isp[row] != 0;
+    double* Wr = W + row * LD + 2 * m;
+    const double* R0 = Rb + m * LD + g;
+    const double* R1 = Rb + (4 + m) * LD + g;
+    for (int tj0 = t0; tj0 < t1; tj0 += 4) {
+      double c0[4], c1[4], b0[4], b1[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int tj = min(tj0 + v, t1 - 1);
+        c0[v] = zr ? 0.0 : Wr[tj * 8];
+        c1[v] = zr ? 0.0 : Wr[tj * 8 + 1];
+        b0[v] = R0[tj * 8];
+        b1[v] = R1[tj * 8];
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) dmma_8x8x4(c0[v], c1[v], a0, b0[v]);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) dmma_8x8x4(c0[v], c1[v], a1, b1[v]);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int tj = tj0 + v;
+        if (tj < t1 && tj != pp && !(skip1 && tj == pp + 1)) {
+          Wr[tj * 8] = c0[v];
+          Wr[tj * 8 + 1] = c1[v];
+        }
+      }
+    }
+  }
+}
+
+template <int S>
+__host__ __device__ constexpr size_t blk_smem_bytes() {
+  // W, two panel buffers, two pivot-row buffers, row scales, panel pivot-row
+  // buffer; ints: perm, posof, two isp flag arrays
+  return sizeof(double) * (size_t(S) * (S + 1) + 2 * size_t(S) * 8 + 2 * 8 * size_t(S + 1) + S + 20) +
+         sizeof(int) * (4 * size_t(S));
+}
+
+template <int S>
+__global__ void __launch_bounds__(256, 1) factor_blk_kernel(
+    const int* __restrict__ plist, int count, const int64_t* __restrict__ off,
+    const int64_t* __restrict__ opoff, double* __restrict__ inv, int* __restrict__ status) {
+  constexpr int NT = 256, NW = NT / 32, LD = S + 1, NB = 8, TT = S / 8, R = (S + 31) / 32;
+  constexpr int NONE = 0x7fffffff;
+  static_assert(S % 8 == 0, "8x8 tiles");
+  extern __shared__ __align__(16) double smem[];
+  double* W = smem;                                  // S x LD
+  double* Pb0 = W + S * LD;                          // 2 x (S x NB)  factored panels
+  double* Rb0 = Pb0 + 2 * S * NB;                    // 2 x (NB x LD) pivot rows
+  double* rs = Rb0 + 2 * NB * LD;                    // S row scales
+  double* pbuf = rs + S;                             // 2 x (NB + 2) panel pivot row + info
+  int* perm = reinterpret_cast<int*>(pbuf + 2 * (NB + 2)); // S  position -> row
+  int* posof = perm + S;                             // S  row -> position
+  int* isp0 = posof + S;                             // 2 x S pivot-row flags
+  __shared__ int pids0[2][NB];
+  __shared__ int s_bad;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+#ifdef VK_FACTOR_TRACE
+  long long trc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tt0;
+#endif
+
+  for (int bb = blockIdx.x; bb < count; bb += gridDim.x) {
+#ifdef VK_FACTOR_TRACE
+    tt0 = clock64();
+#endif
+    const int p = plist[bb];
+    const int s = static_cast<int>(off[p + 1] - off[p]);
+    const int np = (s + NB - 1) / NB;
+    if (t == 0 && bb + static_cast<int>(gridDim.x) < count) {   // next block -> L2
+      const int pn = plist[bb + gridDim.x];
+      const int sn = static_cast<int>(off[pn + 1] - off[pn]);
+      const uint32_t bytes = static_cast<uint32_t>(((sn * sn + 1) & ~1) * sizeof(double));
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(inv + opoff[pn]), "r"(bytes)
+                   : "memory");
+    }
+    const double* src = inv + opoff[p];
+    for (int i0 = warp; i0 < S; i0 += 4 * NW) {        // 4 rows x S/32 loads in flight
+      double v[4][(S + 31) / 32];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int jj = 0; jj < (S + 31) / 32; ++jj) {
+          const int i = i0 + u * NW, j = lane + 32 * jj;
+          v[u][jj] = (i < s && j < s) ? __ldg(src + blk_at(i, j, s)) : (i == j ? 1.0 : 0.0);
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int jj = 0; jj < (S + 31) / 32; ++jj) {
+          const int i = i0 + u * NW, j = lane + 32 * jj;
+          if (i < S && j < S) W[i * LD + j] = v[u][jj];
+        }
+    }
+    for (int i = t; i < 2 * S; i += NT) isp0[i] = 0;
+    if (t == 0) s_bad = 0;
+    __syncthreads();
+    for (int i = warp; i < S; i += NW) {                           // row scales, zero-row guard
+      double m = 0.0;
+      for (int j = lane; j < S; j += 32) m = fmax(m, fabs(W[i * LD + j]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) {
+        rs[i] = m;
+        if (i < s && m == 0.0) s_bad = VK_PATCH_ZERO_ROW;
+      }
+    }
+    __syncthreads();
+    VK_TRACE_ADD(0, tt0);
+    if (s_bad) {
+      if (t == 0) status[p] = s_bad;
+      __syncthreads();
+      continue;
+    }
+    int pos[R];
+    double rsc[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int r = lane + 32 * q;
+      pos[q] = (r < S) ? r : NONE;
+      rsc[q] = (r < S) ? rs[r] : 0.0;
+    }
+#ifdef VK_FACTOR_TRACE
+    tt0 = clock64();
+#endif
+    if (warp == 0) {
+      const int st = factor_panel2<S, R>(W, Pb0, pos, rsc, isp0, pids0[0], pbuf, 0, lane);
+      if (st && lane == 0) s_bad = st;
+    }
+    __syncthreads();
+    if (!s_bad)
+      for (int e = t; e < NB * S; e += NT) Rb0[(e / S) * LD + e % S] = W[pids0[0][e / S] * LD + e % S];
+    __syncthreads();
+    VK_TRACE_ADD(1, tt0);
+    for (int pp = 0; pp < np && !s_bad; ++pp) {
+      const int cur = pp & 1, nxt = cur ^ 1;
+      const double* Pb = Pb0 + cur * S * NB;
+      const double* Rb = Rb0 + cur * NB * LD;
+      const int* isp = isp0 + cur * S;
+      const bool ahead = pp + 1 < np;
+#ifdef VK_FACTOR_TRACE
+      tt0 = clock64();
+#endif
+      if (ahead) {
+        if (warp > 0) {                              // panel pp+1's own column tile first
+          for (int ti = warp - 1; ti < TT; ti += NW - 1) {
+            const int tia[1] = {ti}, tja[1] = {pp + 1};
+            const bool ok[1] = {true};
+            panel_update_tiles<1>(W, LD, Pb, Rb, isp, tia, tja, ok, lane);
+          }
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory");   // ... handed to warp 0
+      }
+      VK_TRACE_ADD(2, tt0);
+#ifdef VK_FACTOR_TRACE
+      tt0 = clock64();
+#endif
+      if (warp == 0) {
+        if (ahead) {
+          const int st = factor_panel2<S, R>(W, Pb0 + nxt * S * NB, pos, rsc, isp0 + nxt * S,
+                                             pids0[nxt], pbuf, (pp + 1) * NB, lane);
+          if (st && lane == 0) s_bad = st;
+        }
+        VK_TRACE_ADD(3, tt0);
+      } else {
+        // warps 1..7: every other column tile except panels pp and pp+1
+#ifndef VK_BLK_NOUPD
+        blk_update<S>(W, Pb, Rb, isp, pp, ahead, warp - 1, NW - 1, lane);
+#endif
+        VK_TRACE_ADD(4, tt0);
+      }
+#ifdef VK_FACTOR_TRACE
+      tt0 = clock64();
+#endif
+      __syncthreads();
+      VK_TRACE_ADD(5, tt0);
+#ifdef VK_FACTOR_TRACE
+      tt0 = clock64();
+#endif
+      if (s_bad) break;                                // block-uniform
+      if (t < NB) isp0[cur * S + pids0[cur][t]] = 0;   // panel pp done
+      if (ahead)                                       // pivot rows of pp+1, fully updated
+        for (int e = t; e < NB * S; e += NT)
+          Rb0[nxt * NB * LD + (e / S) * LD + e % S] = W[pids0[nxt][e / S] * LD + e % S];
+      __syncthreads();
+      VK_TRACE_ADD(6, tt0);
+    }
+    if (s_bad) {
+      if (t == 0) status[p] = s_bad;
+      __syncthreads();
+      continue;
+    }
+#ifdef VK_FACTOR_TRACE
+    tt0 = clock64();
+#endif
+    if (warp == 0) {                                   // row <-> position maps
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int r = lane + 32 * q;
+        if (r < S) {
+          posof[r] = pos[q];
+          perm[pos[q]] = r;
+        }
+      }
+    }
+    __syncthreads();
+    // inverse, column-major, coalesced: Ainv[x][y] = W[perm[x]][posof[y]]
+    double* dst = inv + opoff[p];
+    for (int y = warp; y < s; y += NW) {
+      const int cy = posof[y];
+      for (int x = lane; x < s; x += 32) dst[y * s + x] = W[perm[x] * LD + cy];
+    }
+    if (t == 0) status[p] = VK_PATCH_OK;
+    __syncthreads();
+    VK_TRACE_ADD(7, tt0);
+  }
+#ifdef VK_FACTOR_TRACE
+  if (blockIdx.x == 0 && (t == 0 || t == 32))
+    printf("[blk S=%d t=%d] load+scales %lld prologue %lld coltile+handoff %lld w0-panel %lld "
+           "upd %lld bar1 %lld rcopy+bar2 %lld output %lld (cycles, summed over patches)\n",
+           S, t, trc[0], trc[1], trc[2], trc[3], trc[4], trc[5], trc[6], trc[7]);
+#endif
+}
+
+// VK_FACTOR_BLK=0 keeps factor_dmma_kernel (in-kernel extraction) for the large classes
+bool blk_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("VK_FACTOR_BLK");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // VK_FACTOR_DMMA=0 keeps the register-tiled kernel for the large classes
 bool dmma_enabled() {
   static const bool v = [] {
@@ -1014,14 +1404,6 @@ __global__ void __launch_bounds__(TR * TC, MB) factor_tile_kernel(
 // Staged layout: row-major with stride s; for even s row i is rotated by i
 // (A[i][j] at i s + (j + i) mod s) so that lanes reading one column of
 // consecutive rows hit distinct banks (odd effective stride) in both cases.
-__host__ __device__ __forceinline__ int blk_at(int i, int j, int s) {
-  int c = j;
-  if (!(s & 1)) {
-    c = j + i;
-    if (c >= s) c -= s;
-  }
-  return i * s + c;
-}
 
 constexpr int kXRows = 8;     // patch rows per warp pass in the extraction
 constexpr int kXCols = 128;   // largest block the staged (rows / warp) kernels take
@@ -1622,6 +2004,30 @@ int launch_class(int smax, const int* d_ids, int count, const vk_patches_s* h, c
     }
     return VK_OK;
   }
+  if (!extract_only && smax > 64 && smax <= 128 && dmma_enabled() && blk_enabled()) {
+    cudaError_t e = cudaSuccess;
+#define VK_BLK(S_)                                                                              \
+  do {                                                                                          \
+    auto kern = factor_blk_kernel<S_>;                                                          \
+    const size_t dsm = blk_smem_bytes<S_>();                                                    \
+    e = vk_smem_optin((const void*)kern, int(dsm));                                             \
+    const int grid = std::max(1, std::min(count, vk_resident_blocks((const void*)kern, 256, dsm))); \
+    if (e == cudaSuccess)                                                                       \
+      kern<<<grid, 256, dsm, st>>>(d_ids, count, h->off, h->opoff, h->inv, d_status);          \
+  } while (0)
+    if (smax <= 80) VK_BLK(80);
+    else if (smax <= 96) VK_BLK(96);
+    else if (smax <= 104) VK_BLK(104);
+    else if (smax <= 112) VK_BLK(112);
+    else VK_BLK(128);
+#undef VK_BLK
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      vk::set_error("factor_blk_kernel: %s", cudaGetErrorString(e));
+      return VK_ERR_CUDA;
+    }
+    return VK_OK;
+  }
   if (!extract_only && smax > 64 && smax <= 128 && dmma_enabled()) {
     cudaError_t e = cudaSuccess;
 #define VK_DMMA(S_)                                                                             \
@@ -1912,7 +2318,7 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
   }
   // K2: every block of the staged classes into its operator slot (the staged
   // K3 kernels stream them from there)
-  if (rows_max() > 0) {
+  if (rows_max() > 0 || blk_enabled()) {
     static const bool timing_x = getenv("VK_FACTOR_TIMING") != nullptr;
     cudaEvent_t x0 = nullptr, x1 = nullptr;
     if (timing_x) {
@@ -1920,7 +2326,8 @@ extern "C" int vk_patches_factor(vk_patches_t h, vk_csr_t a, int32_t* status_hos
       cudaEventCreate(&x1);
       cudaEventRecord(x0, 0);
     }
-    const int xst = launch_extract(h, a, 0, h->npatch, rows_max(), h->opoff, 0, h->inv, 0);
+    const int xst = launch_extract(h, a, 0, h->npatch, blk_enabled() ? kXCols : rows_max(),
+                                   h->opoff, 0, h->inv, 0);
     if (xst) return xst;
     if (timing_x) {
       cudaEventRecord(x1, 0);

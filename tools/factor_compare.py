@@ -41,7 +41,7 @@ def main():
         return
     for name in sys.argv[1:] or ["cfg2", "cfg3", "cfg4", "cfg5"]:
         files = {}
-        for tag, env in (("new", {}), ("old", {"VK_FACTOR_ROWS": "0"})):
+        for tag, env in (("new", {}), ("old", {"VK_FACTOR_ROWS": "0", "VK_FACTOR_BLK": "0"})):
             f = f"/tmp/fc_{name}_{tag}.npz"
             t0 = time.time()
             subprocess.run([sys.executable, __file__, "--dump", name, f],
