@@ -1429,16 +1429,24 @@ __global__ void __launch_bounds__(256) extract_blocks_kernel(
     const int s = static_cast<int>(off[p + 1] - base);
     if (s > scut) continue;
     double* o = out + (opoff[p] - obase);
-    for (int i0 = 0; i0 < s; i0 += kXRows) {
-      const int nr = min(kXRows, s - i0);
-      int a0 = 0, len = 0;
-      int64_t e0 = 0;
-      if (lane < nr) {
+    // row metadata of pass i0 (lane u < nr: row i0 + u); the next pass's is
+    // fetched while this pass's entries are in flight
+    auto meta = [&](int i0, int& a0, int& len, int64_t& e0) {
+      a0 = 0;
+      len = 0;
+      e0 = 0;
+      if (lane < min(kXRows, s - i0)) {
         const int r = idx[base + i0 + lane];
         e0 = eoff[base + i0 + lane];
         a0 = ptr[r];
         len = ptr[r + 1] - a0;
       }
+    };
+    int a0, len;
+    int64_t e0;
+    meta(0, a0, len, e0);
+    for (int i0 = 0; i0 < s; i0 += kXRows) {
+      const int nr = min(kXRows, s - i0);
 #pragma unroll
       for (int u = 0; u < kXRows; ++u)
         if (u < nr)
@@ -1457,6 +1465,9 @@ __global__ void __launch_bounds__(256) extract_blocks_kernel(
           vv[u][hh] = ok ? __ldg(val + au + kk) : 0.0;
         }
       }
+      int na0 = 0, nlen = 0;
+      int64_t ne0 = 0;
+      if (i0 + kXRows < s) meta(i0 + kXRows, na0, nlen, ne0);
       __syncwarp();
 #pragma unroll
       for (int u = 0; u < kXRows; ++u)
@@ -1477,6 +1488,9 @@ __global__ void __launch_bounds__(256) extract_blocks_kernel(
         for (int j = lane; j < s; j += 32) o[blk_at(i, j, s)] = B[u * kXCols + j];
       }
       __syncwarp();
+      a0 = na0;
+      len = nlen;
+      e0 = ne0;
     }
   }
 }
