@@ -226,6 +226,9 @@ VK_API int vk_csr_to_dense(vk_csr_t a, double* dense, void* stream);
  *   rv/rg: reference velocity basis values / gradients at the nq points
  *   ([nq][nv][2], [nq][nv][2][2]); pv [nq][np]; cell_xy [ncells][3|4][2] in
  *   reference-map vertex order; piola: H(div) contravariant map.
+ * vk_assemble_load: per cell, the manufactured-forcing load (assembly.py:
+ *   136-172 with the forcing of assembly.py:62-87) as nv (dof, s_i load_i)
+ *   pairs (keys[] = dof); reduce them with vk_coo_to_csr (ncols = 1).
  * vk_assemble_facets: per interior edge the (2nv)^2 block of the H(div)
  *   consistency / symmetry / penalty terms (assembly.py:243-267); rv/rg
  *   [6][nq][nv][..] tables per (local edge slot, aligned); info [ne][6] =
@@ -243,6 +246,10 @@ VK_API int vk_assemble_cells(int32_t ncells, int32_t nq, int32_t nv, int32_t np,
                              const int32_t* vdofs, const double* vscale, const int32_t* pdofs,
                              const double* pscale, int32_t poffset, double viscosity,
                              int64_t ncols, int64_t* keys, double* vals, void* stream);
+VK_API int vk_assemble_load(int32_t ncells, int32_t nq, int32_t nv, int32_t quad, int32_t piola,
+                            const double* w, const double* pts, const double* rv,
+                            const double* cell_xy, const int32_t* vdofs, const double* vscale,
+                            double viscosity, int64_t* keys, double* vals, void* stream);
 VK_API int vk_assemble_facets(int32_t nedges, int32_t nq, int32_t nv, const double* w,
                               const double* rv, const double* rg, const int32_t* info,
                               const double* geo, const double* cell_xy, const int32_t* vdofs,

@@ -71,6 +71,8 @@ SIGNATURES = {
     "vk_csr_to_dense": (C.c_int, [_p, _p, _p]),
     "vk_assemble_cells": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p,
                                     _p, _p, _p, _p, _i32, _f64, _i64, _p, _p, _p]),
+    "vk_assemble_load": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _f64,
+                                   _p, _p, _p]),
     "vk_assemble_facets": (C.c_int, [_i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _f64,
                                      _f64, _i64, _p, _p, _p]),
     "vk_prolong_entries": (C.c_int, [_i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _i64,

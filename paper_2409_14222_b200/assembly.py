@@ -20,9 +20,15 @@ without problem packs.
 * :func:`build_hierarchy` — reference ``mg.build_hierarchy`` (``mg.py:
   177-234``) end to end on the device.
 
-The right-hand side of the manufactured problem is not assembled (the hot
-path and the BASELINE recipe use a seeded load vector):
-``System.rhs`` is None.
+The right-hand side of the manufactured problem (``assembly.py:136-172``
+load with the forcing of ``assembly.py:62-87``, the Dirichlet lift and
+boundary values of ``assembly.py:273-285`` / ``spaces.py:170-220``) is
+assembled too (``System.rhs``, a device vector): the per-cell loads on the
+device (``vk_assemble_load``), reduced in the reference's ``np.add.at``
+order by the same deterministic COO reduction, the lift ``rhs - A @ lift``
+with the unconstrained operator by the bit-exact residual kernel, and the
+Taylor-Hood boundary values by the elements' dual functionals on the host
+(boundary cells only).
 """
 
 from __future__ import annotations
@@ -97,10 +103,41 @@ def _interior_edges(mesh):
     return info, geo
 
 
+def manufactured_velocity(pts):
+    """Reference ``ManufacturedSolution.velocity`` (``assembly.py:65-69``)."""
+    x, y = pts[:, 0], pts[:, 1]
+    return np.column_stack([np.sin(np.pi * x) * np.cos(np.pi * y),
+                            -np.cos(np.pi * x) * np.sin(np.pi * y)])
+
+
+def interpolate_boundary(space: fem.Space, fn) -> np.ndarray:
+    """Reference ``spaces.interpolate`` (``spaces.py:170-200``) restricted to
+    the cells that touch a boundary DoF (the only values ``strong_bc`` keeps):
+    every dual functional applied to ``fn`` on the mapped cell, the last cell
+    in cell order winning for shared DoFs, like the reference's loop."""
+    el = space.element
+    topo, geom = space.mesh
+    pts = np.vstack(el.dof_points)
+    bounds = np.cumsum([0] + [len(p) for p in el.dof_points])
+    coeffs = np.zeros(space.ndof)
+    cells = np.flatnonzero(space.boundary_dof[space.cell_dofs].any(axis=1))
+    for c in cells:
+        verts = geom.vertex_coords[geom.cell_map_vertices[c]]
+        fv = np.asarray(fn(fem.map_points(topo.cell_shape, verts, pts)), dtype=float)
+        if el.mapping == "piola":
+            _, det, inv = fem.cell_jacobians(topo.cell_shape, verts, pts)
+            fv = det[:, None] * np.einsum("qab,qb->qa", inv, fv)
+        for i in range(el.ndof):
+            val = np.sum(el.dof_weights[i] * fv[bounds[i]:bounds[i + 1]])
+            coeffs[space.cell_dofs[c, i]] = val / space.cell_dof_scale[c, i]
+    return coeffs
+
+
 def assemble(mixed: fem.Mixed, config: ProblemConfig | None = None, *,
-             apply_bc: bool = True) -> System:
+             apply_bc: bool = True, rhs: bool = True) -> System:
     """Assembled saddle-point operator on the device (velocity block first,
-    then pressure), strong BCs eliminated with identity rows."""
+    then pressure), strong BCs eliminated with identity rows, and (``rhs``)
+    the manufactured right-hand side with the Dirichlet lift."""
     import torch
     L.require_cuda()
     if config is None:
@@ -151,13 +188,42 @@ def assemble(mixed: fem.Mixed, config: ProblemConfig | None = None, *,
                L.ptr(keep[5]), L.ptr(keep[6]), L.ptr(keep[7]), config.viscosity,
                config.penalty, n, L.ptr(keys[nc * per_cell:]), L.ptr(vals[nc * per_cell:]), st)
     bc = fem.strong_bc(vel) if apply_bc else None
+    b = None
+    if rhs:
+        # load: (dof, s_i load_i) per cell, reduced like the operator's COO
+        # (an n x 1 matrix: duplicates summed in cell order = np.add.at)
+        lk = torch.empty(nc * nv, dtype=torch.int64, device="cuda")
+        lv = torch.empty(nc * nv, dtype=torch.float64, device="cuda")
+        L.call("vk_assemble_load", nc, len(rule.weights), nv, int(shape == "quad"), piola,
+               L.ptr(keep[0]), L.ptr(keep[1]), L.ptr(keep[2]), L.ptr(keep[5]), L.ptr(keep[6]),
+               L.ptr(keep[7]), config.viscosity, L.ptr(lk), L.ptr(lv), st)
+        hl = C.c_void_p()
+        L.call("vk_coo_to_csr", nc * nv, L.ptr(lk), L.ptr(lv), n, 1, 0, 0.0, None, None, None,
+               C.byref(hl))
+        b = DeviceCSR(_handle=hl.value, _shape=(n, 1), _nnz=_nnz(hl)).matvec(
+            torch.ones(1, dtype=torch.float64, device="cuda"))
+        if bc is not None:
+            if mixed.case in ("th-tri", "th-quad"):          # assembly.py:300 (Dirichlet data)
+                values = interpolate_boundary(vel, manufactured_velocity)[bc.indices]
+                bc = fem.StrongBc(bc.indices, values)
+                lift = torch.zeros(n, dtype=torch.float64, device="cuda")
+                lift[_dev(bc.indices, np.int64)] = _dev(values, np.float64)
+                hf = C.c_void_p()                            # unconstrained operator
+                L.call("vk_coo_to_csr", total, L.ptr(keys), L.ptr(vals), n, n, 0, 0.0, None,
+                       None, None, C.byref(hf))
+                full = DeviceCSR(_handle=hf.value, _shape=(n, n), _nnz=_nnz(hf))
+                lifted = torch.empty_like(b)
+                full.residual(b, lift, lifted)               # rhs - matrix @ lift
+                b = lifted
+                del full
+            b[_dev(bc.indices, np.int64)] = _dev(bc.values, np.float64)   # assembly.py:280
     mask = _mask(n, bc.indices) if bc is not None else None
     h = C.c_void_p()
     mp = L.ptr(mask) if mask is not None else None
     L.call("vk_coo_to_csr", total, L.ptr(keys), L.ptr(vals), n, n, 0, 0.0, mp, mp, mp,
            C.byref(h))
     matrix = DeviceCSR(_handle=h.value, _shape=(n, n), _nnz=_nnz(h))
-    return System(matrix, None, mixed, bc)
+    return System(matrix, b, mixed, bc)
 
 
 def _nnz(h):
@@ -291,7 +357,7 @@ def build_hierarchy(case: str, k: int, levels: int, config: ProblemConfig | None
     for i in range(levels + 1):
         mesh = fem.structured_mesh(shape, n0 * 2 ** i)
         mixed = fem.build_mixed(case, mesh, k)
-        system = assemble(mixed, config)
+        system = assemble(mixed, config, rhs=(i == levels))   # the finest level's load
         masked = full = None
         if i > 0:
             prev = lv[-1]

@@ -5,6 +5,7 @@
 //   assembly.py:136-172  cell terms 2 nu (eps u, eps v) and -(div v, p)
 //   assembly.py:230-270  H(div) interior-facet consistency / symmetrisation /
 //                        alpha / h_e tangential-jump penalty
+//   assembly.py:136-172  the load vector of the manufactured forcing
 //   assembly.py:93-129   COO accumulation and summation into CSR
 //   assembly.py:273-285  symmetric strong-BC elimination (identity rows)
 //   mg.py:127-167        build_prolongation (first-occurrence dedup, |v| >
@@ -151,6 +152,77 @@ __global__ void __launch_bounds__(kCellThreads) cell_terms_kernel(CellArgs a) {
       vals[nv * nv + t] = (sq[p] * sv[i]) * b;
       keys[nv * nv + np * nv + t] = (unsigned long long)gv[i] * a.ncols + row_p;
       vals[nv * nv + np * nv + t] = (sv[i] * sq[p]) * b;
+    }
+  }
+}
+
+// Right-hand side of the manufactured problem (assembly.py:136-172, load
+// part): per cell, load_i = sum_q w_q det_q f(x_q) . phi_i(x_q) with
+// f = 2 pi^2 nu (sin(pi x) cos(pi y), -cos(pi x) sin(pi y)) (assembly.py:
+// 62-87), phi_i the pushed-forward velocity basis (identity or Piola); written
+// as (dof, s_i load_i) pairs at fixed positions (cell-major) so the
+// deterministic COO reduction sums them in the reference's np.add.at order.
+struct LoadArgs {
+  int ncells, nq, nv, quad, piola, nvert;
+  const double *w, *pts, *rv;             // w[nq], pts[nq][2], rv[nq][nv][2]
+  const double* cell_xy;
+  const int* vdofs;
+  const double* vscale;
+  double coef;                            // 2 pi^2 nu
+  unsigned long long* keys;
+  double* vals;
+};
+
+__global__ void __launch_bounds__(kCellThreads) load_kernel(LoadArgs a) {
+  extern __shared__ double sm[];
+  const int nq = a.nq, nv = a.nv;
+  double* s_rv = sm;                                  // nq*nv*2
+  double* s_wf = s_rv + nq * nv * 2;                  // nq*2: w det f
+  double* s_j = s_wf + nq * 2;                        // nq*5: J, det (Piola)
+  for (int t = threadIdx.x; t < nq * nv * 2; t += blockDim.x) s_rv[t] = a.rv[t];
+  for (int c = blockIdx.x; c < a.ncells; c += gridDim.x) {
+    __syncthreads();
+    const double* xy = a.cell_xy + int64_t(c) * a.nvert * 2;
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+      const double xi = a.pts[2 * q], eta = a.pts[2 * q + 1];
+      double J[2][2], det, inv[2][2];
+      jacobian(a.quad, xy, xi, eta, J, det, inv);
+      // map_points: v0 + [v1 - v0, v2 - v0] (xi, eta) (+ xi eta (v0 - v1 - v2 + v3))
+      double x = xy[0] + (xi * (xy[2] - xy[0]) + eta * (xy[4] - xy[0]));
+      double y = xy[1] + (xi * (xy[3] - xy[1]) + eta * (xy[5] - xy[1]));
+      if (a.quad) {
+        x += xi * eta * (xy[0] - xy[2] - xy[4] + xy[6]);
+        y += xi * eta * (xy[1] - xy[3] - xy[5] + xy[7]);
+      }
+      double sx, cx, sy, cy;
+      sincos(M_PI * x, &sx, &cx);
+      sincos(M_PI * y, &sy, &cy);
+      const double wd = a.w[q] * det;
+      s_wf[2 * q] = wd * (a.coef * (sx * cy));
+      s_wf[2 * q + 1] = wd * (a.coef * (-(cx * sy)));
+      s_j[5 * q + 0] = J[0][0];
+      s_j[5 * q + 1] = J[0][1];
+      s_j[5 * q + 2] = J[1][0];
+      s_j[5 * q + 3] = J[1][1];
+      s_j[5 * q + 4] = det;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+      double acc = 0.0;
+      for (int q = 0; q < nq; ++q) {
+        double p0 = s_rv[(q * nv + i) * 2], p1 = s_rv[(q * nv + i) * 2 + 1];
+        if (a.piola) {
+          const double* jq = s_j + 5 * q;
+          const double u0 = (jq[0] * p0 + jq[1] * p1) / jq[4];
+          const double u1 = (jq[2] * p0 + jq[3] * p1) / jq[4];
+          p0 = u0;
+          p1 = u1;
+        }
+        acc += s_wf[2 * q] * p0 + s_wf[2 * q + 1] * p1;
+      }
+      const int64_t slot = int64_t(c) * nv + i;
+      a.keys[slot] = (unsigned long long)a.vdofs[slot];
+      a.vals[slot] = a.vscale[slot] * acc;
     }
   }
 }
@@ -371,6 +443,26 @@ extern "C" int vk_assemble_cells(int32_t ncells, int32_t nq, int32_t nv, int32_t
   const int grid = std::min(ncells, vk_resident_blocks((const void*)cell_terms_kernel,
                                                        kCellThreads, smem));
   cell_terms_kernel<<<grid, kCellThreads, smem, vk_stream(stream)>>>(a);
+  VK_CHECK_LAUNCH();
+  return VK_OK;
+}
+
+extern "C" int vk_assemble_load(int32_t ncells, int32_t nq, int32_t nv, int32_t quad,
+                                int32_t piola, const double* w, const double* pts,
+                                const double* rv, const double* cell_xy, const int32_t* vdofs,
+                                const double* vscale, double viscosity, int64_t* keys,
+                                double* vals, void* stream) {
+  VK_REQUIRE(ncells >= 0 && nq > 0 && nv > 0 && w && pts && rv && cell_xy && vdofs && vscale &&
+                 keys && vals,
+             "vk_assemble_load: bad argument");
+  if (ncells == 0) return VK_OK;
+  LoadArgs a{ncells, nq, nv, quad, piola, quad ? 4 : 3, w, pts, rv, cell_xy, vdofs, vscale,
+             2.0 * M_PI * M_PI * viscosity, reinterpret_cast<unsigned long long*>(keys), vals};
+  const size_t smem = sizeof(double) * (size_t(nq) * nv * 2 + size_t(nq) * 7);
+  VK_REQUIRE(smem <= 200 * 1024, "vk_assemble_load: tables too large (%zu bytes)", smem);
+  VK_CHECK_CUDA(vk_smem_optin((const void*)load_kernel, int(smem)));
+  const int grid = std::min(ncells, vk_resident_blocks((const void*)load_kernel, kCellThreads, smem));
+  load_kernel<<<grid, kCellThreads, smem, vk_stream(stream)>>>(a);
   VK_CHECK_LAUNCH();
   return VK_OK;
 }
