@@ -777,7 +777,11 @@ __device__ __forceinline__ int factor_panel2(double* W, double* Pb, int (&pos)[R
     for (int c = 0; c < NB; ++c) pan[q][c] = (r < S) ? W[r * LD + k0 + c] : 0.0;
   }
   int okall = 1;
-#pragma unroll
+  // rotated panel: register 0 always holds the pivot column (the update
+  // writes column c into register c-1 and the pivot column into register
+  // NB-1), so the 8 steps are one compact runtime loop; after NB steps the
+  // frame is the identity again
+#pragma unroll 1
   for (int kk = 0; kk < NB; ++kk) {
     const int k = k0 + kk;
     // this lane's best open row (branch-free): largest |a|, lowest position
@@ -785,7 +789,7 @@ __device__ __forceinline__ int factor_panel2(double* W, double* Pb, int (&pos)[R
     int bpos = NONE, bq = 0;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      const double v = fabs(pan[q][kk]);
+      const double v = fabs(pan[q][0]);
       const bool open = pos[q] >= k && pos[q] < S;
       const bool better = open && (v > bv || (v == bv && pos[q] < bpos));
       bv = better ? v : bv;
@@ -808,9 +812,9 @@ __device__ __forceinline__ int factor_panel2(double* W, double* Pb, int (&pos)[R
       }
     }
     const int wl = __ffs(eq) - 1;
-    // the winner publishes its raw panel row, position, slot and guard verdict;
-    // every lane forms 1/pivot and the scaled row itself (same operations as
-    // the unblocked kernels, so the values are identical)
+    // the winner publishes its raw panel row (rotated frame), position, slot
+    // and guard verdict; every lane forms 1/pivot and the scaled row itself
+    // (same operations as the unblocked kernels, so the values are identical)
     double* pb = pbuf + (kk & 1) * (NB + 2);
     if (lane == wl) {
 #pragma unroll
@@ -819,7 +823,7 @@ __device__ __forceinline__ int factor_panel2(double* W, double* Pb, int (&pos)[R
 #pragma unroll
         for (int c = 0; c < NB; c += 2)
           *reinterpret_cast<double2*>(pb + c) = make_double2(pan[q][c], pan[q][c + 1]);
-        const int ok = fabs(pan[q][kk]) >= 1e-12 * rsc[q];   // sparsela.py:79-83
+        const int ok = fabs(pan[q][0]) >= 1e-12 * rsc[q];    // sparsela.py:79-83
         reinterpret_cast<int*>(pb + NB)[0] = bpos;
         reinterpret_cast<int*>(pb + NB)[1] = q;
         reinterpret_cast<int*>(pb + NB + 1)[0] = ok;
@@ -836,22 +840,24 @@ __device__ __forceinline__ int factor_panel2(double* W, double* Pb, int (&pos)[R
     const int ppos = reinterpret_cast<const int*>(pb + NB)[0];
     const int qw = reinterpret_cast<const int*>(pb + NB)[1];
     okall &= reinterpret_cast<const int*>(pb + NB + 1)[0];
-    const double rinv = __drcp_rn(prow[kk]);           // == 1.0 / pivot (correctly rounded)
+    const double rinv = __drcp_rn(prow[0]);            // == 1.0 / pivot (correctly rounded)
 #pragma unroll
-    for (int c = 0; c < NB; ++c) prow[c] = (c == kk) ? rinv : prow[c] * rinv;
+    for (int c = 1; c < NB; ++c) prow[c] = prow[c] * rinv;
+    prow[0] = rinv;
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      const double f = pan[q][kk];
+      const double f = pan[q][0];
 #pragma unroll
-      for (int c = 0; c < NB; ++c)
-        pan[q][c] = (c == kk) ? -f * rinv : fma(-f, prow[c], pan[q][c]);
+      for (int c = 1; c < NB; ++c) pan[q][c - 1] = fma(-f, prow[c], pan[q][c]);
+      pan[q][NB - 1] = -f * rinv;
     }
     if (lane == wl) {                                  // the pivot row: the scaled row
 #pragma unroll
       for (int q = 0; q < R; ++q)
         if (q == qw) {
 #pragma unroll
-          for (int c = 0; c < NB; ++c) pan[q][c] = prow[c];
+          for (int c = 1; c < NB; ++c) pan[q][c - 1] = prow[c];
+          pan[q][NB - 1] = rinv;
         }
     }
 #pragma unroll
