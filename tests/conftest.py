@@ -28,20 +28,58 @@ _PACKS = {}
 
 
 def load_case(name):
-    """(pack, golden dict) for a named case; full configs skip if absent."""
+    """(pack, golden dict) for a named case.  Full configs: the full-size
+    golden in data/ when present, else the committed compact stand-in
+    tests/golden/<name>_compact.npz (tools/compact_golden.py: hashes, whole
+    small arrays, sampled N-vectors); skip only if neither or no pack."""
     if name in _PACKS:
         return _PACKS[name]
     from paper_2409_14222_b200.pack import read_pack
     pp, gp = case_paths(name)
-    for p in (pp, gp):
-        if not os.path.exists(p):
-            pytest.skip(f"{p} not present (generate with tools/make_packs.py)")
+    if not os.path.exists(pp):
+        pytest.skip(f"{pp} not present (generate with tools/make_packs.py)")
+    if not os.path.exists(gp) or os.environ.get("VK_COMPACT_GOLDEN") == "1":
+        cp = os.path.join(GOLDEN, f"{name}_compact.npz")
+        if not os.path.exists(cp):
+            pytest.skip(f"{gp} not present (generate with tools/make_packs.py)")
+        gp = cp
     g = dict(np.load(gp))
     hp = os.path.join(GOLDEN, f"{name}_history.json")
     if os.path.exists(hp):
         g["info"] = json.load(open(hp))
     _PACKS[name] = (read_pack(pp), g)
     return _PACKS[name]
+
+
+def golden_same(g, key, actual) -> bool:
+    """Bit-equality of ``actual`` with the golden array ``key`` (float arrays
+    compared as bit patterns); against its SHA-256 in a compact golden."""
+    import hashlib
+    if key in g:
+        ref = np.asarray(g[key])
+        a = np.ascontiguousarray(actual, dtype=ref.dtype)
+        return a.shape == ref.shape and a.tobytes() == np.ascontiguousarray(ref).tobytes()
+    a = np.ascontiguousarray(actual, dtype=np.dtype(str(g[key + "__dtype"])))
+    if tuple(a.shape) != tuple(int(v) for v in g[key + "__shape"]):
+        return False
+    return hashlib.sha256(a.tobytes()).hexdigest() == str(g[key + "__sha256"])
+
+
+def golden_rel(g, key, actual) -> float:
+    """||actual - ref|| / ||ref|| against the golden N-vector ``key``.  Compact
+    golden: the same ratio over the stored sample positions, or the relative
+    difference of the full 2-norms / max-abs if that is larger."""
+    actual = np.asarray(actual)
+    if key in g:
+        ref = g[key]
+        return float(np.linalg.norm(actual - ref) / np.linalg.norm(ref))
+    assert len(actual) == int(g[key + "__len"])
+    idx, val = g[key + "__idx"], g[key + "__val"]
+    rel = np.linalg.norm(actual[idx] - val) / np.linalg.norm(val)
+    nrm = float(g[key + "__norm"])
+    mx = float(g[key + "__maxabs"])
+    return float(max(rel, abs(np.linalg.norm(actual) - nrm) / nrm,
+                     abs(np.abs(actual).max() - mx) / mx))
 
 
 def seeded_residual(n, seed):
