@@ -264,6 +264,34 @@ VK_API int vk_coo_to_csr(int64_t n, int64_t* keys, double* vals, int32_t nrows, 
                          int32_t dup_first, double drop_abs, const uint8_t* row_drop,
                          const uint8_t* col_drop, const uint8_t* diag_one, vk_csr_t* out);
 
+/* ---------------- discretisation-error measurement --------------------------
+ * replaces the reference's bench.error_norms (bench.py:95-164) for the
+ * manufactured enclosed-flow solution (assembly.py:55-87), called by
+ * run_case / stopping_study (bench.py:174-191, 239-301).
+ * vk_error_cells: per (cell, quadrature point) of the degree min(2k+4, 20)
+ *   rule: w det (|u_h - u|^2 + |grad u_h - grad u|^2), w det (|u|^2 +
+ *   |grad u|^2), |div u_h|, p_h and w det into work[5][ncells*nq]; tables and
+ *   maps as for vk_assemble_cells, x the solution vector (pressure block at
+ *   poffset).
+ * vk_error_jump: per (interior edge, point) w_q [u_h . t]^2 / 2 (the
+ *   tangential-jump seminorm integrand, bench.py:143-158) into
+ *   work[nedges*nq]; rv/info/geo as for vk_assemble_facets.
+ * vk_error_reduce: fixed-order single-CTA reduction; out[6] (device) = sum
+ *   e2, sum base, max |div|, sum w (p - mean)^2, sum of the jump terms, mean
+ *   pressure.  All stream-ordered, asynchronous. */
+VK_API int vk_error_cells(int32_t ncells, int32_t nq, int32_t nv, int32_t np, int32_t quad,
+                          int32_t piola, const double* w, const double* pts, const double* rv,
+                          const double* rg, const double* pv, const double* cell_xy,
+                          const int32_t* vdofs, const double* vscale, const int32_t* pdofs,
+                          const double* pscale, int32_t poffset, const double* x, double* work,
+                          void* stream);
+VK_API int vk_error_jump(int32_t nedges, int32_t nq, int32_t nv, const double* w, const double* rv,
+                         const int32_t* info, const double* geo, const double* cell_xy,
+                         const int32_t* vdofs, const double* vscale, const double* x,
+                         double* work, void* stream);
+VK_API int vk_error_reduce(int64_t ncq, const double* work, int64_t neq, const double* jump,
+                           double* out, void* stream);
+
 /* ---------------- coarse dense operator and its inverse --------------------
  * replaces the reference's coarse factorization (mg.py:228-232:
  * lu_factor(A0.toarray() + shift * np.outer(q, q))), applied per V-cycle as

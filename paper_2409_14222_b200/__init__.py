@@ -2,7 +2,8 @@
 
 Drop-in for the hot path of the reference package ``stokesmg``
 (arXiv 2409.14222 companion code): the names below mirror
-``stokesmg/__init__.py:29-35`` for ``sparsela``, ``vanka`` and ``mg``.  All
+``stokesmg/__init__.py:15-35`` for ``sparsela``, ``vanka``, ``mg``, the
+assembly entry points and the ``bench`` driver layer (``experiments.py``).  All
 numerics run in ``libvanka_b200.so`` (hand-written CUDA behind a C ABI,
 ``include/vanka_b200.h``); importing works without a GPU, computing does not
 (no CPU fallback).
@@ -21,5 +22,7 @@ from .mg import (ChebyshevParams, FixedDamping, Level, MgHierarchy, TransferPair
                  hierarchy_from_reference, make_preconditioner, pressure_kernel, v_cycle)
 from .assembly import ProblemConfig, assemble, build_hierarchy, build_prolongation
 from .fem import build_mixed, strong_bc, structured_mesh
+from .experiments import (RunRecord, RunSpec, error_norms, expand_grid, run_case, stopping_study,
+                          sweep)
 
 __version__ = "0.1.0"

@@ -79,6 +79,10 @@ SIGNATURES = {
                                      _i64, _p, _p, _p]),
     "vk_coo_to_csr": (C.c_int, [_i64, _p, _p, _i32, _i32, _i32, _f64, _p, _p, _p,
                                 C.POINTER(_p)]),
+    "vk_error_cells": (C.c_int, [_i32, _i32, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p,
+                                 _p, _p, _p, _i32, _p, _p, _p]),
+    "vk_error_jump": (C.c_int, [_i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "vk_error_reduce": (C.c_int, [_i64, _p, _i64, _p, _p, _p]),
     "vk_coarse_operator": (C.c_int, [_p, _p, _f64, _p, _p]),
     "vk_dense_inverse_workspace": (C.c_int64, [_i32]),
     "vk_dense_inverse": (C.c_int, [_i32, _p, _p, _p, _P_i32, _P_i32, _p]),

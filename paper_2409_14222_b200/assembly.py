@@ -103,6 +103,27 @@ def _interior_edges(mesh):
     return info, geo
 
 
+def facet_tables(vel: fem.Space):
+    """Interior-edge data of an H(div) velocity space: (info, geo) of
+    :func:`_interior_edges`, the edge quadrature of degree 2 deg + 2
+    (``assembly.py:194``) and the element's reference tabulation on each
+    (local edge slot, orientation) — six tables, points matched by arc length
+    along the global edge direction like ``jump_average_tables``
+    (``assembly.py:188-226``)."""
+    info, geo = _interior_edges(vel.mesh)
+    erule = fem.quadrature("interval", 2 * vel.element.degree + 2)
+    s = erule.points[:, 0]
+    tabs_v, tabs_g = [], []
+    for la, lb in fem.TRI_SLOTS:
+        for aligned in (0, 1):
+            a, b = (fem.TRI_REF[la], fem.TRI_REF[lb]) if aligned else \
+                (fem.TRI_REF[lb], fem.TRI_REF[la])
+            tv, tg = vel.element.tabulate(a + s[:, None] * (b - a))
+            tabs_v.append(tv)
+            tabs_g.append(tg)
+    return info, geo, erule, tabs_v, tabs_g
+
+
 def manufactured_velocity(pts):
     """Reference ``ManufacturedSolution.velocity`` (``assembly.py:65-69``)."""
     x, y = pts[:, 0], pts[:, 1]
@@ -156,17 +177,7 @@ def assemble(mixed: fem.Mixed, config: ProblemConfig | None = None, *,
     per_cell = nv * nv + 2 * npl * nv
     facets = mixed.case in ("bdm", "rt")
     if facets:
-        info, geo = _interior_edges(vel.mesh)
-        erule = fem.quadrature("interval", 2 * vel.element.degree + 2)  # assembly.py:194
-        s = erule.points[:, 0]
-        tabs_v, tabs_g = [], []
-        for la, lb in fem.TRI_SLOTS:
-            for aligned in (0, 1):
-                a, b = (fem.TRI_REF[la], fem.TRI_REF[lb]) if aligned else \
-                    (fem.TRI_REF[lb], fem.TRI_REF[la])
-                tv, tg = vel.element.tabulate(a + s[:, None] * (b - a))
-                tabs_v.append(tv)
-                tabs_g.append(tg)
+        info, geo, erule, tabs_v, tabs_g = facet_tables(vel)
         nfe = len(info)
     else:
         nfe = 0

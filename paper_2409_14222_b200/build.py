@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libvanka_b200.so")
 SOURCES = ["vk_csr.cu", "vk_patches.cu", "vk_factor.cu", "vk_apply.cu", "vk_blas.cu",
-           "vk_dense.cu", "vk_assembly.cu"]
+           "vk_dense.cu", "vk_assembly.cu", "vk_errors.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

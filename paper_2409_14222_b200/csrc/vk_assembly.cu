@@ -26,52 +26,11 @@
 #include <cub/cub.cuh>
 
 #include "vk_common.cuh"
+#include "vk_fem.cuh"
 
 namespace {
 
 constexpr int kCellThreads = 256;
-
-// per-quadrature-point Jacobian of the affine (tri) / bilinear (quad) map
-__device__ __forceinline__ void jacobian(int quad, const double* __restrict__ xy, double x,
-                                         double y, double J[2][2], double& det, double inv[2][2]) {
-  const double x0 = xy[0], y0 = xy[1];
-  J[0][0] = xy[2] - x0;
-  J[1][0] = xy[3] - y0;
-  J[0][1] = xy[4] - x0;
-  J[1][1] = xy[5] - y0;
-  if (quad) {
-    const double tx = x0 - xy[2] - xy[4] + xy[6], ty = y0 - xy[3] - xy[5] + xy[7];
-    J[0][0] += y * tx;
-    J[1][0] += y * ty;
-    J[0][1] += x * tx;
-    J[1][1] += x * ty;
-  }
-  det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
-  inv[0][0] = J[1][1] / det;
-  inv[0][1] = -J[0][1] / det;
-  inv[1][0] = -J[1][0] / det;
-  inv[1][1] = J[0][0] / det;
-}
-
-// physical gradient (c, a) and value (c) of reference basis function data
-// rv[c], rg[c][d] under the identity (gradients by J^-T) or Piola map
-__device__ __forceinline__ void push(int piola, const double J[2][2], double det,
-                                     const double inv[2][2], const double rv[2],
-                                     const double rg[2][2], double pv[2], double pg[2][2]) {
-  if (!piola) {
-    pv[0] = rv[0];
-    pv[1] = rv[1];
-    for (int c = 0; c < 2; ++c)
-      for (int a = 0; a < 2; ++a) pg[c][a] = rg[c][0] * inv[0][a] + rg[c][1] * inv[1][a];
-    return;
-  }
-  for (int c = 0; c < 2; ++c) pv[c] = (J[c][0] * rv[0] + J[c][1] * rv[1]) / det;
-  double jg[2][2];
-  for (int c = 0; c < 2; ++c)
-    for (int b = 0; b < 2; ++b) jg[c][b] = J[c][0] * rg[0][b] + J[c][1] * rg[1][b];
-  for (int c = 0; c < 2; ++c)
-    for (int a = 0; a < 2; ++a) pg[c][a] = (jg[c][0] * inv[0][a] + jg[c][1] * inv[1][a]) / det;
-}
 
 struct CellArgs {
   int ncells, nq, nv, np, quad, piola, nvert, poffset;
@@ -187,13 +146,8 @@ __global__ void __launch_bounds__(kCellThreads) load_kernel(LoadArgs a) {
       const double xi = a.pts[2 * q], eta = a.pts[2 * q + 1];
       double J[2][2], det, inv[2][2];
       jacobian(a.quad, xy, xi, eta, J, det, inv);
-      // map_points: v0 + [v1 - v0, v2 - v0] (xi, eta) (+ xi eta (v0 - v1 - v2 + v3))
-      double x = xy[0] + (xi * (xy[2] - xy[0]) + eta * (xy[4] - xy[0]));
-      double y = xy[1] + (xi * (xy[3] - xy[1]) + eta * (xy[5] - xy[1]));
-      if (a.quad) {
-        x += xi * eta * (xy[0] - xy[2] - xy[4] + xy[6]);
-        y += xi * eta * (xy[1] - xy[3] - xy[5] + xy[7]);
-      }
+      double x, y;
+      map_point(a.quad, xy, xi, eta, x, y);
       double sx, cx, sy, cy;
       sincos(M_PI * x, &sx, &cx);
       sincos(M_PI * y, &sy, &cy);

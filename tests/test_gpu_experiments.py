@@ -1,0 +1,117 @@
+"""Experiment-driver layer on the device against the unmodified reference
+(tests/golden/bench_golden.*, tools/make_bench_golden.py): ``error_norms`` of
+the reference's own solution vectors, ``run_case`` end to end on device-built
+hierarchies (reference-default Chebyshev bounds), ``sweep`` and
+``stopping_study``."""
+
+import io
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+REL_NORM = 1e-10         # error_norms of the same vector: summation order only
+DIV_NOISE = 1e-9         # H(div) pairs: max |div u_h| is rounding noise (~1e-11)
+
+
+@pytest.fixture(scope="module")
+def golden():
+    meta = json.load(open(os.path.join(GOLDEN, "bench_golden.json")))
+    return meta, np.load(os.path.join(GOLDEN, "bench_golden.npz"))
+
+
+def _mixed(case, k, levels):
+    from paper_2409_14222_b200 import fem, mg
+    shape = "quad" if case == "th-quad" else "tri"
+    mesh = fem.structured_mesh(shape, mg.COARSE_CELLS_PER_SIDE * 2 ** levels)
+    return fem.build_mixed(case, mesh, k)
+
+
+def _check_norms(got, ref, hdiv):
+    for i in (0, 1, 3):
+        assert abs(got[i] - ref[i]) <= REL_NORM * abs(ref[i]) + 1e-300, (i, got, ref)
+    # max |div u_h| is a cancelling sum of O(pi) gradient entries: rounding of
+    # ~1e-14 absolute on top of the relative gate
+    assert abs(got[2] - ref[2]) <= (DIV_NOISE if hdiv else REL_NORM * ref[2] + 1e-12)
+
+
+RUNS = ["th-tri_2_1_2", "th-tri_3_1_1", "th-quad_2_1_2", "th-quad_3_2_2", "bdm_1_1_2",
+        "bdm_2_1_2", "rt_1_1_2", "rt_2_2_1"]
+
+
+@pytest.mark.parametrize("name", RUNS)
+def test_error_norms_of_reference_solutions(name, golden, capsys):
+    import torch
+    import paper_2409_14222_b200 as V
+    meta, arr = golden
+    run = next(r for r in meta["runs"] if r["name"] == name)
+    mixed = _mixed(run["case"], run["k"], run["levels"])
+    hdiv = run["case"] in ("bdm", "rt")
+    got = V.error_norms(arr[name + "_x"], mixed)
+    _check_norms(got, arr[name + "_norms_x"], hdiv)
+    # a perturbed vector, explicit quadrature degree, device input
+    y = torch.from_numpy(arr[name + "_y"]).cuda()
+    got_y = V.error_norms(y, mixed, 1.0, 2 * run["k"] + 1)
+    _check_norms(got_y, arr[name + "_norms_y"], False)
+    with capsys.disabled():
+        ref = arr[name + "_norms_x"]
+        print(f"\n[{name}] error norms rel diff "
+              f"{[abs(g - r) / max(abs(r), 1e-300) for g, r in zip(got, ref)]}")
+    with pytest.raises(ValueError):
+        V.error_norms(arr[name + "_x"][:-1], mixed)
+
+
+@pytest.mark.parametrize("name", RUNS)
+def test_run_case_matches_reference(name, golden, capsys):
+    import paper_2409_14222_b200 as V
+    meta, _ = golden
+    run = next(r for r in meta["runs"] if r["name"] == name)
+    spec = V.RunSpec(run["case"], run["k"], nu=run["nu"], levels=run["levels"])
+    rec = V.run_case(spec)
+    with capsys.disabled():
+        print(f"\n[{name}] {rec.csv_row()}\n{' ' * (len(name) + 3)}{run['csv_row']}")
+    assert (rec.n_dofs, rec.m_dofs) == (run["n_dofs"], run["m_dofs"])
+    assert rec.converged == run["converged"]
+    assert abs(rec.iterations - run["iterations"]) <= 1
+    for key in ("err_h1_vel_rel", "err_l2_p_abs", "jump_seminorm"):
+        assert abs(getattr(rec, key) - run[key]) <= 1e-6 * abs(run[key]) + 1e-300, key
+    if run["case"] in ("bdm", "rt"):
+        assert rec.max_div <= 1e-9
+    else:
+        assert abs(rec.max_div - run["max_div"]) <= 1e-6 * run["max_div"]
+    # identical leading CSV fields (case .. rtol, iterations when equal)
+    assert rec.csv_row().split(",")[:9] == run["csv_row"].split(",")[:9]
+
+
+def test_sweep_streams_rows_and_reuses_hierarchies():
+    import paper_2409_14222_b200 as V
+    out = io.StringIO()
+    specs = V.expand_grid({"case": "th-quad", "k": 2, "nu": [1, 2], "levels": 1, "rtol": 1e-8})
+    recs = V.sweep(specs, out)
+    lines = out.getvalue().strip().split("\n")
+    assert lines[0] == V.experiments.CSV_COLUMNS and len(lines) == 3
+    assert recs[0].setup_s > 0.0 and recs[1].setup_s == 0.0       # one build, first use
+    assert all(r.converged for r in recs)
+    assert recs[1].iterations <= recs[0].iterations
+
+
+@pytest.mark.parametrize("idx", [0, 1])
+def test_stopping_study_matches_reference(idx, golden, capsys):
+    import paper_2409_14222_b200 as V
+    meta, _ = golden
+    study = meta["stopping"][idx]
+    out = io.StringIO()
+    rows = V.stopping_study(study["case"], study["k"], study["max_levels"], out=out)
+    with capsys.disabled():
+        print("\n" + out.getvalue() + study["csv"])
+    assert len(rows) == len(study["rows"])
+    for row, (levels, rtol, verr, perr, ok) in zip(rows, study["rows"]):
+        assert (row.levels, row.resolved) == (levels, ok)
+        assert row.required_rtol == rtol
+        assert abs(row.err_h1_vel_rel - verr) <= 1e-6 * verr
+        assert abs(row.err_l2_p_abs - perr) <= 1e-6 * perr
