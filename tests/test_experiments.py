@@ -77,3 +77,22 @@ def test_stopping_row_format_and_case_check():
             assert row.csv_row() == line
     with pytest.raises(ValueError, match="covers th-quad and bdm only"):
         stopping_study("th-tri", 2, 1)
+
+
+def test_cli_parses_reference_flags():
+    """Same subcommands / flags / defaults as the reference front end
+    (cli.py:22-64)."""
+    from paper_2409_14222_b200.__main__ import _parser
+    p = _parser()
+    a = p.parse_args("run --case rt --k 2 --out r.csv".split())
+    assert (a.nu, a.levels, a.rtol, a.max_it, a.alpha, a.viscosity, a.seed, a.weighting,
+            a.cheby) == (2, 1, 1e-10, 100, None, 1.0, 0, "invmult", "repeat")
+    a = p.parse_args("run --case bdm --k 3 --max-it 7 --alpha 2.5 --cheby degree --out r.csv"
+                     .split())
+    assert (a.max_it, a.alpha, a.cheby) == (7, 2.5, "degree")
+    a = p.parse_args("stopping --case th-quad --k 2 --max-levels 3 --out s.csv".split())
+    assert (a.nu, a.seed, a.max_levels) == (1, 0, 3)
+    for bad in ("run --case dg --k 2 --out r.csv", "run --case bdm --out r.csv",
+                "stopping --case th-tri --k 2 --max-levels 1 --out s.csv", "sweep --out s.csv"):
+        with pytest.raises(SystemExit):
+            p.parse_args(bad.split())

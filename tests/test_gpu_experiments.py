@@ -115,3 +115,21 @@ def test_stopping_study_matches_reference(idx, golden, capsys):
         assert row.required_rtol == rtol
         assert abs(row.err_h1_vel_rel - verr) <= 1e-6 * verr
         assert abs(row.err_l2_p_abs - perr) <= 1e-6 * perr
+
+
+def test_cli_run_and_sweep(tmp_path, golden, capsys):
+    from paper_2409_14222_b200.__main__ import main
+    import paper_2409_14222_b200 as V
+    meta, _ = golden
+    run = next(r for r in meta["runs"] if r["name"] == "bdm_1_1_2")
+    out = tmp_path / "run.csv"
+    assert main(["run", "--case", "bdm", "--k", "1", "--out", str(out)]) == 0
+    header, row = out.read_text().strip().split("\n")
+    assert header == V.experiments.CSV_COLUMNS
+    assert row.split(",")[:11] == run["csv_row"].split(",")[:11]       # .. iterations, converged
+    cfg = tmp_path / "grid.toml"
+    cfg.write_text('case = "th-tri"\nk = 2\nnu = [1, 2]\nlevels = 1\nrtol = 1e-8\n')
+    out2 = tmp_path / "sweep.csv"
+    assert main(["sweep", "--config", str(cfg), "--out", str(out2)]) == 0
+    assert len(out2.read_text().strip().split("\n")) == 3
+    assert "wrote 2 rows" in capsys.readouterr().out
