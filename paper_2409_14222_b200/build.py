@@ -49,11 +49,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         flags += ["-Xptxas", "-v"]
     flags += os.environ.get("VK_NVCC_FLAGS", "").split()  # experiments only
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")] + \
+        [os.path.join(ROOT, "include", "vanka_b200.h")]
+    stamp = os.path.join(tmp, "flags.txt")
+    same_flags = os.path.exists(stamp) and open(stamp).read() == " ".join(flags)
     for src in SOURCES:
         obj = os.path.join(tmp, src.replace(".cu", ".o"))
+        objs.append(obj)
+        deps = [os.path.join(CSRC, src), *headers]
+        if not force and same_flags and os.path.exists(obj) and \
+                all(os.path.getmtime(d) < os.path.getmtime(obj) for d in deps):
+            continue                       # object is newer than its source and every header
         cmd = [nvcc(), *flags, "-c", os.path.join(CSRC, src), "-o", obj]
         subprocess.run(cmd, check=True)
-        objs.append(obj)
+    with open(stamp, "w") as fh:
+        fh.write(" ".join(flags))
     cmd = [nvcc(), *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart"]
     subprocess.run(cmd, check=True)
     os.replace(LIB + ".tmp", LIB)
