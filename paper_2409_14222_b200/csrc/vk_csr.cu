@@ -329,6 +329,79 @@ __global__ void __launch_bounds__(kStreamThreads) csr_pipe_kernel(
   }
 }
 
+// Bulk-copy form of the stream kernel (VK_SPMV_MODE=3): the block's (col,
+// val) chunk arrives in shared memory by two TMA bulk copies (L2 -> smem, no
+// L1 / LSU traffic, no per-thread load instructions), so the L1 t-stage — the
+// busiest unit of csr_stream_kernel (64%) — only serves the x gathers; the
+// products overwrite val in place.  Bulk copies need 16-byte aligned sources
+// and sizes: the chunk starts at k0 rounded down to a multiple of 4 entries
+// and its length is rounded up (the arrays are padded by 8 entries).
+template <int MODE>
+__global__ void __launch_bounds__(kStreamThreads) csr_bulk_kernel(
+    const int2* __restrict__ blk, const int* __restrict__ ptr, const int* __restrict__ col,
+    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+    double alpha, double beta, const double* __restrict__ b) {
+  __shared__ __align__(128) double sval[kStreamNnz + 8];
+  __shared__ __align__(16) int scol[kStreamNnz + 8];
+  __shared__ int sptr[kStreamRows + 1];
+  __shared__ uint64_t bar;
+  pdl_trigger();
+  const int t = threadIdx.x;
+  const int2 e0 = blk[blockIdx.x], e1 = blk[blockIdx.x + 1];
+  const int r0 = e0.x, k0 = e0.y, k1 = e1.y, nr = e1.x - r0;
+  const int ka = k0 & ~3, off = k0 - ka, cnt = (k1 - ka + 3) & ~3;
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    const uint64_t pol = evict_first_policy();
+    mbar_expect_tx(&bar, uint32_t(cnt) * 12u);
+    if (cnt) {
+      bulk_g2s(sval, val + ka, uint32_t(cnt) * 8u, &bar, pol);
+      bulk_g2s(scol, col + ka, uint32_t(cnt) * 4u, &bar, pol);
+    }
+  }
+  for (int i = t; i <= nr; i += kStreamThreads) cp_async4(sptr + i, ptr + r0 + i);
+  __syncthreads();                  // barrier initialised before anyone waits on it
+  pdl_wait();
+  mbar_wait(&bar, 0);
+  double* prod = sval + off;
+  const int* sc = scol + off;
+  const int n = k1 - k0;
+#pragma unroll
+  for (int u = 0; u < kStreamU; ++u) {
+    const int k = t + u * kStreamThreads;
+    if (k < n) prod[k] = __dmul_rn(prod[k], __ldg(x + sc[k]));
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  for (int i0 = 0; i0 < nr; i0 += kStreamThreads) {
+    const int i = i0 + t;
+    const int lane = t & 31;
+    int a = 0, len = 0;
+    if (i < nr) {
+      a = sptr[i] - k0;
+      len = sptr[i + 1] - k0 - a;
+    }
+    const int d = len > 0 ? (a - lane) & 15 : 0;
+    const int steps = __reduce_max_sync(0xffffffffu, len > 0 ? len + d : 0);
+    double s = 0.0;
+#pragma unroll 4
+    for (int st = 0; st < steps; ++st) {
+      const int k = st - d;
+      if (k >= 0 && k < len) s = __dadd_rn(s, prod[a + k]);
+    }
+    if (i >= nr) continue;
+    const int row = r0 + i;
+    if (MODE == 1) {
+      y[row] = __dsub_rn(b[row], s);
+    } else {
+      double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
+      if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[row] : __dmul_rn(beta, y[row]), out);
+      y[row] = out;
+    }
+  }
+}
+
 // Builds the staged-x schedule of one row block: sort the block's columns,
 // compact the distinct ones (ascending) into ucol[k0 ..], and give every
 // nonzero its position in that list.
@@ -561,6 +634,9 @@ cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alp
   const int mode = spmv_mode();
   if (mode != 0 && a.max_row <= kStreamNnz) {
     const int64_t bytes = 12 * a.nnz + 24 * int64_t(a.nrows);
+    if (mode == 3)
+      return vk_launch(csr_bulk_kernel<MODE>, dim3(a.nblocks), dim3(kStreamThreads), 0, st, bytes,
+                       a.blk, a.indptr, a.indices, a.data, x, y, alpha, beta, b);
     if (mode == 2 && a.ucol) {
       const int grid = std::min(a.nblocks, vk_resident_blocks(
           (const void*)csr_pipe_kernel<MODE, true>, kStreamThreads, 0));
@@ -666,8 +742,11 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
   a->nnz = nnz;
   a->nblocks = static_cast<int32_t>(rb.size()) - 1;
   e = cudaMalloc(&a->indptr, sizeof(int32_t) * (nrows + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&a->indices, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
-  if (e == cudaSuccess) e = cudaMalloc(&a->data, sizeof(double) * std::max<int64_t>(nnz, 1));
+  // + 8 entries: the bulk-copy kernel reads whole 16-byte groups past a block's end
+  if (e == cudaSuccess) e = cudaMalloc(&a->indices, sizeof(int32_t) * (nnz + 8));
+  if (e == cudaSuccess) e = cudaMalloc(&a->data, sizeof(double) * (nnz + 8));
+  if (e == cudaSuccess) e = cudaMemset(a->indices + nnz, 0, sizeof(int32_t) * 8);
+  if (e == cudaSuccess) e = cudaMemset(a->data + nnz, 0, sizeof(double) * 8);
   std::vector<int2> bt(rb.size());
   for (size_t i = 0; i < rb.size(); ++i) bt[i] = make_int2(rb[i], hp[rb[i]]);
   if (e == cudaSuccess) e = cudaMalloc(&a->blk, sizeof(int2) * bt.size());
