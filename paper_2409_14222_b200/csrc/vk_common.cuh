@@ -33,13 +33,6 @@ struct Csr {
   // CSR-stream schedule: row blocks of <= kStreamNnz nonzeros / kStreamRows rows
   int32_t nblocks = 0;
   int2* blk = nullptr;         // [nblocks+1] (first row, first nonzero) of each block
-  // staged-x schedule (csr_staged_kernel): per row block the sorted unique
-  // columns (ucol[k0 .. k0 + ucnt[b])) and every nonzero's position in that
-  // list (loc); built on the device at creation when every block fits one
-  // chunk and the matrix takes the stream kernel
-  int32_t* ucol = nullptr;     // [nnz]
-  uint16_t* loc = nullptr;     // [nnz]
-  int32_t* ucnt = nullptr;     // [nblocks]
   uint64_t uid = 0;            // process-unique id of this (immutable) sparsity pattern
 };
 

@@ -22,8 +22,6 @@
 #include <string>
 
 #include <cooperative_groups.h>
-#include <cub/cub.cuh>
-#include <climits>
 
 #include "vk_common.cuh"
 
@@ -193,265 +191,6 @@ __global__ void __launch_bounds__(kStreamThreads) csr_stream_kernel(
                                  carry);
 }
 
-// Software-pipelined persistent form of the stream kernel (and, with
-// STAGED, of its staged-x variant).  csr_stream_kernel's CTA does load ->
-// gather -> barrier -> row sums strictly in sequence, so while a CTA sums its
-// rows (a few dozen active threads) it has nothing in flight; the SM covers
-// that only with other resident CTAs and ends up latency-bound (ncu: 36
-// cycles per issued instruction, DRAM at 56%).  Here a CTA walks the block
-// table with stride gridDim.x and issues the operator loads of its NEXT block
-// (into registers; row pointers by cp.async into the other sptr buffer) right
-// after the products of the current one are in shared memory, so HBM loads
-// stay in flight through the barrier and the row sums.
-//
-// STAGED: each block's distinct columns are listed once (ucol, built at
-// creation), the CTA gathers x at those columns into shared memory — one
-// load per distinct column instead of one per nonzero (a 2048-nonzero block
-// touches only 200-700 distinct columns) — and the products read x from there
-// through 2-byte local indices; HBM bytes per nonzero 8 (val) + 2 (loc) +
-// 4 distinct / nnz (ucol) ~ 10.4-11.3 instead of 12.
-//
-// Same products, same left-to-right row sums as csr_stream_kernel:
-// bit-identical.  Requires every block to fit one chunk (no row longer than
-// kStreamNnz).
-template <int MODE, bool STAGED>
-__global__ void __launch_bounds__(kStreamThreads) csr_pipe_kernel(
-    int nblocks, const int2* __restrict__ blk, const int* __restrict__ ptr,
-    const int* __restrict__ col, const int* __restrict__ ucol, const int* __restrict__ ucnt,
-    const uint16_t* __restrict__ loc, const double* __restrict__ val,
-    const double* __restrict__ x, double* __restrict__ y, double alpha, double beta,
-    const double* __restrict__ b) {
-  __shared__ double prod[kStreamNnz];
-  __shared__ double xs[STAGED ? kStreamNnz : 1];
-  __shared__ int sptr[2][kStreamRows + 1];
-  pdl_trigger();
-  const int t = threadIdx.x;
-  constexpr int UX = 4;
-  int c[kStreamU];        // column (stream) or local index (staged)
-  double v[kStreamU];
-  int uc[STAGED ? UX : 1];
-  int bi = blockIdx.x;
-  if (bi >= nblocks) return;
-  int2 e0 = blk[bi], e1 = blk[bi + 1];
-  int nu = STAGED ? ucnt[bi] : 0;
-  // loads of one block: registers + row pointers into sptr[buf]
-  auto issue = [&](int2 f0, int2 f1, int nuq, int buf) {
-    const int nrq = f1.x - f0.x;
-    for (int i = t; i <= nrq; i += kStreamThreads) cp_async4(&sptr[buf][i], ptr + f0.x + i);
-    if (STAGED) {
-#pragma unroll
-      for (int u = 0; u < UX; ++u) {
-        const int j = t + u * kStreamThreads;
-        uc[u] = (j < nuq) ? __ldcs(ucol + f0.y + j) : 0;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kStreamU; ++u) {
-      const int k = f0.y + t + u * kStreamThreads;
-      if (STAGED) c[u] = (k < f1.y) ? int(__ldcs(loc + k)) : 0;
-      else c[u] = (k < f1.y) ? __ldcs(col + k) : 0;
-      v[u] = (k < f1.y) ? __ldcs(val + k) : 0.0;
-    }
-  };
-  issue(e0, e1, nu, 0);
-  pdl_wait();
-  int buf = 0;
-  while (true) {
-    const int r0 = e0.x, k0 = e0.y, k1 = e1.y, nr = e1.x - r0;
-    if (STAGED) {
-#pragma unroll
-      for (int u = 0; u < UX; ++u) {
-        const int j = t + u * kStreamThreads;
-        if (j < nu) xs[j] = __ldg(x + uc[u]);
-      }
-      for (int j = t + UX * kStreamThreads; j < nu; j += kStreamThreads)
-        xs[j] = __ldg(x + __ldcs(ucol + k0 + j));
-      __syncthreads();
-#pragma unroll
-      for (int u = 0; u < kStreamU; ++u) {
-        const int k = t + u * kStreamThreads;
-        if (k0 + k < k1) prod[k] = __dmul_rn(v[u], xs[c[u]]);
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < kStreamU; ++u) {
-        const int k = t + u * kStreamThreads;
-        if (k0 + k < k1) prod[k] = __dmul_rn(v[u], __ldg(x + c[u]));
-      }
-    }
-    cp_async_wait_all();            // this block's row pointers
-    // next block's loads fly during the barrier and the row sums
-    const int bn = bi + gridDim.x;
-    int2 n0 = e0, n1 = e1;
-    int nun = 0;
-    if (bn < nblocks) {
-      n0 = blk[bn];
-      n1 = blk[bn + 1];
-      nun = STAGED ? ucnt[bn] : 0;
-      issue(n0, n1, nun, buf ^ 1);
-    }
-    __syncthreads();
-    // one thread per row, left-to-right sums with the bank skew of stream_block
-    const int* sp = sptr[buf];
-    for (int i0 = 0; i0 < nr; i0 += kStreamThreads) {
-      const int i = i0 + t;
-      const int lane = t & 31;
-      int a = 0, len = 0;
-      if (i < nr) {
-        a = sp[i] - k0;
-        len = sp[i + 1] - k0 - a;
-      }
-      const int d = len > 0 ? (a - lane) & 15 : 0;
-      const int steps = __reduce_max_sync(0xffffffffu, len > 0 ? len + d : 0);
-      double s = 0.0;
-#pragma unroll 4
-      for (int st = 0; st < steps; ++st) {
-        const int k = st - d;
-        if (k >= 0 && k < len) s = __dadd_rn(s, prod[a + k]);
-      }
-      if (i >= nr) continue;
-      const int row = r0 + i;
-      if (MODE == 1) {
-        y[row] = __dsub_rn(b[row], s);
-      } else {
-        double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
-        if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[row] : __dmul_rn(beta, y[row]), out);
-        y[row] = out;
-      }
-    }
-    if (bn >= nblocks) break;
-    __syncthreads();                // prod / xs are rewritten by the next block
-    bi = bn;
-    e0 = n0;
-    e1 = n1;
-    nu = nun;
-    buf ^= 1;
-  }
-}
-
-// Bulk-copy form of the stream kernel (VK_SPMV_MODE=3): the block's (col,
-// val) chunk arrives in shared memory by two TMA bulk copies (L2 -> smem, no
-// L1 / LSU traffic, no per-thread load instructions), so the L1 t-stage — the
-// busiest unit of csr_stream_kernel (64%) — only serves the x gathers; the
-// products overwrite val in place.  Bulk copies need 16-byte aligned sources
-// and sizes: the chunk starts at k0 rounded down to a multiple of 4 entries
-// and its length is rounded up (the arrays are padded by 8 entries).
-template <int MODE>
-__global__ void __launch_bounds__(kStreamThreads) csr_bulk_kernel(
-    const int2* __restrict__ blk, const int* __restrict__ ptr, const int* __restrict__ col,
-    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-    double alpha, double beta, const double* __restrict__ b) {
-  __shared__ __align__(128) double sval[kStreamNnz + 8];
-  __shared__ __align__(16) int scol[kStreamNnz + 8];
-  __shared__ int sptr[kStreamRows + 1];
-  __shared__ uint64_t bar;
-  pdl_trigger();
-  const int t = threadIdx.x;
-  const int2 e0 = blk[blockIdx.x], e1 = blk[blockIdx.x + 1];
-  const int r0 = e0.x, k0 = e0.y, k1 = e1.y, nr = e1.x - r0;
-  const int ka = k0 & ~3, off = k0 - ka, cnt = (k1 - ka + 3) & ~3;
-  if (t == 0) {
-    mbar_init(&bar, 1);
-    mbar_fence_init();
-    const uint64_t pol = evict_first_policy();
-    mbar_expect_tx(&bar, uint32_t(cnt) * 12u);
-    if (cnt) {
-      bulk_g2s(sval, val + ka, uint32_t(cnt) * 8u, &bar, pol);
-      bulk_g2s(scol, col + ka, uint32_t(cnt) * 4u, &bar, pol);
-    }
-  }
-  for (int i = t; i <= nr; i += kStreamThreads) cp_async4(sptr + i, ptr + r0 + i);
-  __syncthreads();                  // barrier initialised before anyone waits on it
-  pdl_wait();
-  mbar_wait(&bar, 0);
-  double* prod = sval + off;
-  const int* sc = scol + off;
-  const int n = k1 - k0;
-#pragma unroll
-  for (int u = 0; u < kStreamU; ++u) {
-    const int k = t + u * kStreamThreads;
-    if (k < n) prod[k] = __dmul_rn(prod[k], __ldg(x + sc[k]));
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  for (int i0 = 0; i0 < nr; i0 += kStreamThreads) {
-    const int i = i0 + t;
-    const int lane = t & 31;
-    int a = 0, len = 0;
-    if (i < nr) {
-      a = sptr[i] - k0;
-      len = sptr[i + 1] - k0 - a;
-    }
-    const int d = len > 0 ? (a - lane) & 15 : 0;
-    const int steps = __reduce_max_sync(0xffffffffu, len > 0 ? len + d : 0);
-    double s = 0.0;
-#pragma unroll 4
-    for (int st = 0; st < steps; ++st) {
-      const int k = st - d;
-      if (k >= 0 && k < len) s = __dadd_rn(s, prod[a + k]);
-    }
-    if (i >= nr) continue;
-    const int row = r0 + i;
-    if (MODE == 1) {
-      y[row] = __dsub_rn(b[row], s);
-    } else {
-      double out = (alpha == 1.0) ? s : __dmul_rn(alpha, s);
-      if (beta != 0.0) out = __dadd_rn(beta == 1.0 ? y[row] : __dmul_rn(beta, y[row]), out);
-      y[row] = out;
-    }
-  }
-}
-
-// Builds the staged-x schedule of one row block: sort the block's columns,
-// compact the distinct ones (ascending) into ucol[k0 ..], and give every
-// nonzero its position in that list.
-__global__ void __launch_bounds__(kStreamThreads) stage_build_kernel(
-    const int2* __restrict__ blk, const int* __restrict__ col, int* __restrict__ ucol,
-    uint16_t* __restrict__ loc, int* __restrict__ ucnt) {
-  using Sort = cub::BlockRadixSort<int, kStreamThreads, kStreamU>;
-  using Scan = cub::BlockScan<int, kStreamThreads>;
-  __shared__ union {
-    typename Sort::TempStorage sort;
-    typename Scan::TempStorage scan;
-  } tmp;
-  __shared__ int sorted[kStreamNnz];
-  __shared__ int uniq[kStreamNnz];
-  const int t = threadIdx.x, bi = blockIdx.x;
-  const int k0 = blk[bi].y, n = blk[bi + 1].y - k0;
-  int keys[kStreamU];
-#pragma unroll
-  for (int u = 0; u < kStreamU; ++u) {
-    const int j = t * kStreamU + u;
-    keys[u] = (j < n) ? col[k0 + j] : INT_MAX;
-  }
-  Sort(tmp.sort).Sort(keys);
-#pragma unroll
-  for (int u = 0; u < kStreamU; ++u) sorted[t * kStreamU + u] = keys[u];
-  __syncthreads();
-  int flag[kStreamU], pos[kStreamU], total;
-#pragma unroll
-  for (int u = 0; u < kStreamU; ++u) {
-    const int j = t * kStreamU + u;
-    flag[u] = (keys[u] != INT_MAX) && (j == 0 || sorted[j - 1] != keys[u]);
-  }
-  Scan(tmp.scan).ExclusiveSum(flag, pos, total);
-#pragma unroll
-  for (int u = 0; u < kStreamU; ++u)
-    if (flag[u]) uniq[pos[u]] = keys[u];
-  __syncthreads();
-  for (int j = t; j < total; j += kStreamThreads) ucol[k0 + j] = uniq[j];
-  if (t == 0) ucnt[bi] = total;
-  for (int j = t; j < n; j += kStreamThreads) {
-    const int c = col[k0 + j];
-    int lo = 0, hi = total - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (uniq[mid] < c) lo = mid + 1; else hi = mid;
-    }
-    loc[k0 + j] = static_cast<uint16_t>(lo);
-  }
-}
-
 // Short-row kernel (thread per row): for matrices with a few nonzeros per
 // row (prolongations) the shared-memory staging of the stream kernel costs
 // more than it saves.  Same per-row operation order (sequential, FMA-free).
@@ -611,16 +350,6 @@ cudaError_t launch_tree(const vk::Csr& a, const double* x, double* y, double alp
 #undef VK_TREE
 }
 
-// VK_SPMV_MODE: 0 = csr_stream_kernel, 1 = pipelined (default), 2 = pipelined
-// + staged x (A/B measurements; all three are bit-identical)
-static int spmv_mode() {
-  static const int v = [] {
-    const char* e = getenv("VK_SPMV_MODE");
-    return e ? atoi(e) : 1;
-  }();
-  return v;
-}
-
 template <int MODE>
 cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alpha, double beta,
                         const double* b, cudaStream_t st) {
@@ -630,25 +359,6 @@ cudaError_t launch_spmv(const vk::Csr& a, const double* x, double* y, double alp
     return vk_launch(csr_row_kernel<MODE>, dim3((a.nrows + 255) / 256), dim3(256), 0, st,
                      12 * a.nnz + 24 * int64_t(a.nrows), a.nrows, a.indptr, a.indices, a.data,
                      x, y, alpha, beta, b);
-  }
-  const int mode = spmv_mode();
-  if (mode != 0 && a.max_row <= kStreamNnz) {
-    const int64_t bytes = 12 * a.nnz + 24 * int64_t(a.nrows);
-    if (mode == 3)
-      return vk_launch(csr_bulk_kernel<MODE>, dim3(a.nblocks), dim3(kStreamThreads), 0, st, bytes,
-                       a.blk, a.indptr, a.indices, a.data, x, y, alpha, beta, b);
-    if (mode == 2 && a.ucol) {
-      const int grid = std::min(a.nblocks, vk_resident_blocks(
-          (const void*)csr_pipe_kernel<MODE, true>, kStreamThreads, 0));
-      return vk_launch(csr_pipe_kernel<MODE, true>, dim3(grid), dim3(kStreamThreads), 0, st, bytes,
-                       a.nblocks, a.blk, a.indptr, a.indices, a.ucol, a.ucnt, a.loc, a.data, x, y,
-                       alpha, beta, b);
-    }
-    const int grid = std::min(a.nblocks, vk_resident_blocks(
-        (const void*)csr_pipe_kernel<MODE, false>, kStreamThreads, 0));
-    return vk_launch(csr_pipe_kernel<MODE, false>, dim3(grid), dim3(kStreamThreads), 0, st, bytes,
-                     a.nblocks, a.blk, a.indptr, a.indices, a.ucol, a.ucnt, a.loc, a.data, x, y,
-                     alpha, beta, b);
   }
   return vk_launch(csr_stream_kernel<MODE>, dim3(a.nblocks), dim3(kStreamThreads), 0, st,
                    12 * a.nnz + 24 * int64_t(a.nrows), a.blk, a.indptr, a.indices, a.data, x, y,
@@ -742,11 +452,8 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
   a->nnz = nnz;
   a->nblocks = static_cast<int32_t>(rb.size()) - 1;
   e = cudaMalloc(&a->indptr, sizeof(int32_t) * (nrows + 1));
-  // + 8 entries: the bulk-copy kernel reads whole 16-byte groups past a block's end
-  if (e == cudaSuccess) e = cudaMalloc(&a->indices, sizeof(int32_t) * (nnz + 8));
-  if (e == cudaSuccess) e = cudaMalloc(&a->data, sizeof(double) * (nnz + 8));
-  if (e == cudaSuccess) e = cudaMemset(a->indices + nnz, 0, sizeof(int32_t) * 8);
-  if (e == cudaSuccess) e = cudaMemset(a->data + nnz, 0, sizeof(double) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&a->indices, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+  if (e == cudaSuccess) e = cudaMalloc(&a->data, sizeof(double) * std::max<int64_t>(nnz, 1));
   std::vector<int2> bt(rb.size());
   for (size_t i = 0; i < rb.size(); ++i) bt[i] = make_int2(rb[i], hp[rb[i]]);
   if (e == cudaSuccess) e = cudaMalloc(&a->blk, sizeof(int2) * bt.size());
@@ -779,24 +486,6 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
     wsum += m;
   }
   a->warp_max_mean = ng ? wsum / ng : 0.0;
-  // staged-x schedule for the matrices the stream kernel serves (every block
-  // one chunk: no row longer than kStreamNnz)
-  if (spmv_mode() == 2 && nnz && a->warp_max_mean > VK_CSR_SHORT && mx <= kStreamNnz) {
-    e = cudaMalloc(&a->ucol, sizeof(int32_t) * nnz);
-    if (e == cudaSuccess) e = cudaMalloc(&a->loc, sizeof(uint16_t) * nnz);
-    if (e == cudaSuccess) e = cudaMalloc(&a->ucnt, sizeof(int32_t) * a->nblocks);
-    if (e == cudaSuccess) {
-      stage_build_kernel<<<a->nblocks, kStreamThreads>>>(a->blk, a->indices, a->ucol, a->loc,
-                                                         a->ucnt);
-      e = cudaGetLastError();
-      if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    }
-    if (e != cudaSuccess) {
-      vk::set_error("vk_csr_create (staged schedule): %s", cudaGetErrorString(e));
-      vk_csr_destroy(a);
-      return VK_ERR_CUDA;
-    }
-  }
   *out = a;
   return VK_OK;
 }
@@ -842,9 +531,6 @@ extern "C" int vk_csr_destroy(vk_csr_t a) {
   cudaFree(a->indices);
   cudaFree(a->data);
   cudaFree(a->blk);
-  cudaFree(a->ucol);
-  cudaFree(a->loc);
-  cudaFree(a->ucnt);
   delete a;
   return VK_OK;
 }
