@@ -419,108 +419,6 @@ __global__ void __launch_bounds__(256) gemm_sub_kernel(int mrows, int ncols, int
   }
 }
 
-// The same update for the large (K >= 64) trailing / substitution GEMMs that
-// carry almost all of the 2 n^3 flops: 128 x 128 tile per CTA, 256 threads
-// as 16 x 16, 8 x 8 outputs per thread (two 4-row groups 64 apart and four
-// 2-column groups 32 apart, so the operand reads are 16-byte shared loads:
-// broadcast for A, 256 contiguous bytes per half-warp for B), K in chunks of 16, the next chunk prefetched into
-// registers while the current one is multiplied, double-buffered shared
-// tiles.  64 DFMAs per 8 LDS.128 per thread and k instead of 16 per 8 scalar
-// loads: the shared-memory operand traffic that bounds gemm_sub_kernel (4 x 4
-// outputs per thread) drops 4x per flop.  Every output is still the chain
-// acc = fma(a_is, b_sj, acc) over s ascending from zero, subtracted from C
-// once: bit-identical to gemm_sub_kernel.
-constexpr int kGM = 128, kGN = 128, kGK = 16;
-__global__ void __launch_bounds__(256, 1) gemm_sub_big_kernel(
-    int mrows, int ncols, int K, const double* __restrict__ A, int64_t lda,
-    const double* __restrict__ B, int64_t ldb, double* __restrict__ Cm, int64_t ldc,
-    const int* __restrict__ status) {
-  extern __shared__ __align__(16) double gsm[];
-  // [2][kGK][kGM + 2] (A transposed: [s][row], +2: the transposing stores of
-  // a thread pair land in different banks) and [2][kGK][kGN]
-  constexpr int AS = kGM + 2;
-  double* As = gsm;
-  double* Bs = gsm + 2 * kGK * AS;
-  if (__ldcg(status)) return;
-  const int t = threadIdx.x;
-  const int tx = t & 15, ty = t >> 4;
-  const int i0 = blockIdx.y * kGM, j0 = blockIdx.x * kGN;
-  // loader roles: A: row t/2, k half (t&1)*8 .. +8;  B: k t/16, columns (t%16)*8 .. +8
-  const int ar = t >> 1, ak = (t & 1) * 8;
-  const int bk = t >> 4, bc = (t & 15) * 8;
-  const bool arow_ok = i0 + ar < mrows;
-  const double* ap = A + int64_t(i0 + ar) * lda + ak;
-  double pa[8], pbv[8];
-  auto fetch = [&](int s0) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      pa[u] = (arow_ok && s0 + ak + u < K) ? __ldg(ap + s0 + u) : 0.0;
-    const bool brow_ok = s0 + bk < K;
-    const double* bp = B + int64_t(s0 + bk) * ldb + j0 + bc;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) pbv[u] = (brow_ok && j0 + bc + u < ncols) ? __ldg(bp + u) : 0.0;
-  };
-  auto stash = [&](int buf) {
-    double* as = As + buf * kGK * AS;
-    double* bs = Bs + buf * kGK * kGN;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) as[(ak + u) * AS + ar] = pa[u];
-#pragma unroll
-    for (int u = 0; u < 8; u += 2)
-      *reinterpret_cast<double2*>(bs + bk * kGN + bc + u) = make_double2(pbv[u], pbv[u + 1]);
-  };
-  double acc[8][8];
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[a][q] = 0.0;
-  fetch(0);
-  stash(0);
-  __syncthreads();
-  int buf = 0;
-  for (int s0 = 0; s0 < K; s0 += kGK) {
-    const bool more = s0 + kGK < K;
-    if (more) fetch(s0 + kGK);
-    const double* as = As + buf * kGK * AS;
-    const double* bs = Bs + buf * kGK * kGN;
-    const int kc = min(kGK, K - s0);
-#pragma unroll 4
-    for (int s = 0; s < kc; ++s) {
-      double av[8], bv[8];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const double2 a01 = *reinterpret_cast<const double2*>(as + s * AS + h * 64 + ty * 4);
-        const double2 a23 = *reinterpret_cast<const double2*>(as + s * AS + h * 64 + ty * 4 + 2);
-        av[h * 4 + 0] = a01.x; av[h * 4 + 1] = a01.y; av[h * 4 + 2] = a23.x; av[h * 4 + 3] = a23.y;
-      }
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {     // 16 lanes x 16 B contiguous: conflict-free
-        const double2 b01 = *reinterpret_cast<const double2*>(bs + s * kGN + g * 32 + tx * 2);
-        bv[g * 2 + 0] = b01.x; bv[g * 2 + 1] = b01.y;
-      }
-#pragma unroll
-      for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[a][q] = fma(av[a], bv[q], acc[a][q]);
-    }
-    if (more) {
-      stash(buf ^ 1);
-      __syncthreads();
-      buf ^= 1;
-    }
-  }
-#pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int i = i0 + (a >> 2) * 64 + ty * 4 + (a & 3);
-    if (i >= mrows) continue;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int j = j0 + (q >> 1) * 32 + tx * 2 + (q & 1);
-      if (j < ncols) Cm[i * ldc + j] = __dsub_rn(Cm[i * ldc + j], acc[a][q]);
-    }
-  }
-}
-
 __global__ void identity_kernel(int n, double* __restrict__ x) {
   const int64_t total = int64_t(n) * n;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
@@ -608,21 +506,6 @@ int panel_grid() {
 cudaError_t gemm_sub(int mrows, int ncols, int nbk, const double* A, int64_t lda, const double* B,
                      int64_t ldb, double* Cm, int64_t ldc, const int* status, cudaStream_t st) {
   if (mrows <= 0 || ncols <= 0) return cudaSuccess;
-  // big tiles when they fill the machine and K amortises the prologue
-  static const bool big_ok = [] {
-    const char* e = getenv("VK_GEMM_BIG");
-    return !(e && e[0] == '0');
-  }();
-  const int64_t tiles = int64_t((ncols + kGN - 1) / kGN) * ((mrows + kGM - 1) / kGM);
-  if (big_ok && nbk >= 64 && tiles >= 148) {
-    constexpr size_t smem = sizeof(double) * 2 * kGK * (kGM + 2 + kGN);
-    cudaError_t e = vk_smem_optin((const void*)gemm_sub_big_kernel, int(smem));
-    if (e != cudaSuccess) return e;
-    const dim3 grid((ncols + kGN - 1) / kGN, (mrows + kGM - 1) / kGM);
-    gemm_sub_big_kernel<<<grid, 256, smem, st>>>(mrows, ncols, nbk, A, lda, B, ldb, Cm, ldc,
-                                                 status);
-    return cudaGetLastError();
-  }
   const dim3 grid((ncols + kBN - 1) / kBN, (mrows + kBM - 1) / kBM);
   gemm_sub_kernel<<<grid, 256, 0, st>>>(mrows, ncols, nbk, A, lda, B, ldb, Cm, ldc, status);
   return cudaGetLastError();
