@@ -229,6 +229,29 @@ def extract_submatrix(a, rows, cols):
     return out.cpu().numpy()
 
 
+# largest block the batched patch kernels take; above it lu_factor uses the
+# dense coarse-operator path (same LAPACK pivot order, same guard)
+_PATCH_KERNEL_MAX = 128
+
+
+def _dense_inverse(a: np.ndarray):
+    """(explicit inverse on the device, guard status) of a large dense matrix
+    by the hand-written blocked LU (``vk_dense_inverse``)."""
+    import ctypes as C
+    torch = _torch()
+    n = a.shape[0]
+    m = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    work = torch.empty(max(int(L.lib().vk_dense_inverse_workspace(n)), 1), dtype=torch.uint8,
+                       device="cuda")
+    inv = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    reason, col = C.c_int32(0), C.c_int32(-1)
+    rc = L.call("vk_dense_inverse", n, L.ptr(m), L.ptr(inv), L.ptr(work), C.byref(reason),
+                C.byref(col), _stream())
+    if rc == L.VK_SINGULAR:
+        return None, int(reason.value)
+    return inv, 0
+
+
 def lu_factor(a) -> DenseFactorization:
     """Dense factorization with partial pivoting and the reference guard
     (``sparsela.py:63-84``), on the device: one-patch Gauss-Jordan with the
@@ -239,7 +262,10 @@ def lu_factor(a) -> DenseFactorization:
         raise ValueError("need a square matrix")
     if a.shape[0] == 0:
         return DenseFactorization(None, None, (0, 0), None)
-    inv, status = _single_block_inverse(a)
+    if a.shape[0] > _PATCH_KERNEL_MAX:
+        inv, status = _dense_inverse(a)      # blocked LU + inverse (vk_dense_inverse)
+    else:
+        inv, status = _single_block_inverse(a)
     if status == L.VK_PATCH_ZERO_ROW:
         raise SingularMatrixError("matrix has an all-zero row")
     if status == L.VK_PATCH_SMALL_PIVOT:
