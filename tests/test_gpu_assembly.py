@@ -143,3 +143,98 @@ def test_mg_fgmres_on_device_built_hierarchy(name, capsys):
               f"{floor:.2e})")
     assert conv and its == int(g["iterations"])
     assert rel <= max(1e-9, 10 * floor)
+
+
+# ---------------------------------------------------------------------------
+# property tests of the reference's tests/test_assembly.py on the device
+# assembly (same meshes, same conditions)
+# ---------------------------------------------------------------------------
+
+def system_for(case, k, n, apply_bc=True, **cfg):
+    from paper_2409_14222_b200 import ProblemConfig, assemble, fem
+    mesh = fem.structured_mesh("quad" if case == "th-quad" else "tri", n)
+    mixed = fem.build_mixed(case, mesh, k)
+    config = ProblemConfig(case, k, **cfg)
+    return assemble(mixed, config, apply_bc=apply_bc), mixed, config
+
+
+def sym_error(mat):
+    diff = (mat - mat.T).tocoo()
+    scale = np.max(np.abs(mat.data)) if mat.nnz else 1.0
+    return (np.max(np.abs(diff.data)) / scale) if diff.nnz else 0.0
+
+
+# reference tests/test_assembly.py:68-74, 131-134
+@pytest.mark.parametrize("case,k,n", [("th-tri", 2, 3), ("th-quad", 3, 2), ("bdm", 1, 2),
+                                      ("bdm", 2, 2), ("rt", 2, 2)])
+def test_symmetry_and_zero_pressure_block(case, k, n):
+    system, mixed, _ = system_for(case, k, n)
+    mat = system.matrix.to_scipy()
+    assert sym_error(mat) < 1e-10
+    pp = mat[mixed.offset:, mixed.offset:]
+    assert pp.nnz == 0 or np.max(np.abs(pp.data)) == 0.0
+
+
+# reference tests/test_assembly.py:76-83
+def test_constrained_rows_identity():
+    system, mixed, _ = system_for("th-tri", 2, 2)
+    mat = system.matrix.to_scipy().tocsr()
+    rhs = system.rhs.cpu().numpy()
+    for pos, idx in enumerate(system.bc.indices[:10]):
+        row = mat.getrow(idx)
+        assert row.nnz == 1 and row.indices[0] == idx
+        assert row.data[0] == 1.0
+        assert rhs[idx] == system.bc.values[pos]
+
+
+# reference tests/test_assembly.py:85-91
+def test_rigid_translation_in_kernel_of_raw_a():
+    import paper_2409_14222_b200 as V
+    system, mixed, _ = system_for("th-quad", 2, 2, apply_bc=False)
+    const = np.zeros(mixed.ndof)
+    const[0:mixed.offset:2] = 1.0   # unit x-translation
+    out = V.spmv(system.matrix, const)
+    assert np.max(np.abs(out[:mixed.offset])) < 1e-12
+
+
+# reference tests/test_assembly.py:93-99, 211-224
+@pytest.mark.parametrize("case,k,cfg,sign", [("th-tri", 2, {}, +1), ("bdm", 1, {}, +1),
+                                             ("bdm", 1, {"alpha": 0.01}, -1)])
+def test_velocity_block_definiteness(case, k, cfg, sign):
+    system, mixed, _ = system_for(case, k, 2, **cfg)
+    free = np.setdiff1d(np.arange(mixed.offset), system.bc.indices)
+    a_free = system.matrix.to_scipy().tocsr()[free][:, free].toarray()
+    lo = np.linalg.eigvalsh(a_free).min()
+    assert lo > 1e-12 if sign > 0 else lo < -1e-8     # low penalty loses coercivity
+
+
+# reference tests/test_assembly.py:101-107, 136-143
+@pytest.mark.parametrize("case,k", [("th-tri", 2), ("th-quad", 2), ("bdm", 1), ("rt", 1)])
+def test_constant_pressure_kernel(case, k):
+    import paper_2409_14222_b200 as V
+    system, mixed, _ = system_for(case, k, 3)
+    vec = np.zeros(mixed.ndof)
+    vec[mixed.offset:] = 1.0
+    out = V.spmv(system.matrix, vec)
+    scale = float(np.max(np.abs(system.matrix.to_scipy().data)))
+    assert np.max(np.abs(out)) < 1e-12 * scale
+
+
+# reference tests/test_assembly.py:109-127
+def test_rhs_matches_independent_quadrature():
+    from paper_2409_14222_b200 import fem
+    from paper_2409_14222_b200.assembly import manufactured_velocity
+    system, mixed, _ = system_for("th-tri", 2, 2, apply_bc=False)
+    vel = mixed.velocity
+    topo, geom = vel.mesh
+    rule = fem.quadrature("tri", 6)
+    tab = vel.element.tabulate(rule.points)
+    expected = np.zeros(vel.ndof)
+    for c in range(topo.num_cells):
+        verts = geom.vertex_coords[geom.cell_map_vertices[c]]
+        vals, _ = fem.push_forward(vel.element, "tri", verts, rule.points, tab)
+        _, det, _ = fem.cell_jacobians("tri", verts, rule.points)
+        f = 2.0 * np.pi ** 2 * manufactured_velocity(fem.map_points("tri", verts, rule.points))
+        load = np.einsum("q,qv,qiv->i", rule.weights * det, f, vals)
+        np.add.at(expected, vel.cell_dofs[c], vel.cell_dof_scale[c] * load)
+    assert np.allclose(system.rhs.cpu().numpy()[:vel.ndof], expected, atol=1e-12)
