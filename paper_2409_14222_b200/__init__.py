@@ -20,7 +20,8 @@ from .vanka import (EntityRef, Patch, PatchSet, SweepStream, apply_additive, bui
 from .mg import (ChebyshevParams, FixedDamping, Level, MgHierarchy, TransferPair,
                  chebyshev_iteration, chebyshev_relax, coarse_solve, hierarchy_from_pack,
                  hierarchy_from_reference, make_preconditioner, pressure_kernel, v_cycle)
-from .assembly import ProblemConfig, assemble, build_hierarchy, build_prolongation
+from .assembly import (ProblemConfig, assemble, build_hierarchy, build_prolongation,
+                       interpolate)
 from .fem import build_mixed, strong_bc, structured_mesh
 from .experiments import (RunRecord, RunSpec, error_norms, expand_grid, run_case, stopping_study,
                           sweep)

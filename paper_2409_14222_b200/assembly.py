@@ -131,17 +131,19 @@ def manufactured_velocity(pts):
                             -np.cos(np.pi * x) * np.sin(np.pi * y)])
 
 
-def interpolate_boundary(space: fem.Space, fn) -> np.ndarray:
-    """Reference ``spaces.interpolate`` (``spaces.py:170-200``) restricted to
-    the cells that touch a boundary DoF (the only values ``strong_bc`` keeps):
-    every dual functional applied to ``fn`` on the mapped cell, the last cell
-    in cell order winning for shared DoFs, like the reference's loop."""
+def interpolate(space: fem.Space, fn, *, boundary_only: bool = False) -> np.ndarray:
+    """Reference ``spaces.interpolate`` (``spaces.py:170-200``): every dual
+    functional applied to ``fn`` on the mapped cell, the last cell in cell
+    order winning for shared DoFs, like the reference's loop.
+    ``boundary_only``: just the cells that touch a boundary DoF (the only
+    values ``strong_bc`` keeps)."""
     el = space.element
     topo, geom = space.mesh
     pts = np.vstack(el.dof_points)
     bounds = np.cumsum([0] + [len(p) for p in el.dof_points])
     coeffs = np.zeros(space.ndof)
-    cells = np.flatnonzero(space.boundary_dof[space.cell_dofs].any(axis=1))
+    cells = np.flatnonzero(space.boundary_dof[space.cell_dofs].any(axis=1)) if boundary_only \
+        else np.arange(topo.num_cells)
     for c in cells:
         verts = geom.vertex_coords[geom.cell_map_vertices[c]]
         fv = np.asarray(fn(fem.map_points(topo.cell_shape, verts, pts)), dtype=float)
@@ -152,6 +154,10 @@ def interpolate_boundary(space: fem.Space, fn) -> np.ndarray:
             val = np.sum(el.dof_weights[i] * fv[bounds[i]:bounds[i + 1]])
             coeffs[space.cell_dofs[c, i]] = val / space.cell_dof_scale[c, i]
     return coeffs
+
+
+def interpolate_boundary(space: fem.Space, fn) -> np.ndarray:
+    return interpolate(space, fn, boundary_only=True)
 
 
 def assemble(mixed: fem.Mixed, config: ProblemConfig | None = None, *,

@@ -133,3 +133,90 @@ def test_cli_run_and_sweep(tmp_path, golden, capsys):
     assert main(["sweep", "--config", str(cfg), "--out", str(out2)]) == 0
     assert len(out2.read_text().strip().split("\n")) == 3
     assert "wrote 2 rows" in capsys.readouterr().out
+
+
+# ---------------------------------------------------------------------------
+# the reference's own tests/test_bench.py, same conditions, on the device
+# ---------------------------------------------------------------------------
+
+def _space(case, n, k):
+    from paper_2409_14222_b200 import fem
+    return fem.build_mixed(case, fem.structured_mesh("quad" if case == "th-quad" else "tri", n), k)
+
+
+def _interp_solution(mixed):
+    import paper_2409_14222_b200 as V
+    from paper_2409_14222_b200.assembly import manufactured_velocity
+    x = np.zeros(mixed.ndof)
+    x[:mixed.offset] = V.interpolate(mixed.velocity, manufactured_velocity)
+    return x
+
+
+# reference tests/test_bench.py:22-50
+def test_error_norm_properties():
+    import paper_2409_14222_b200 as V
+    errs = []
+    for n in (5, 10):
+        mixed = _space("th-tri", n, 2)
+        verr, _, _, jump = V.error_norms(_interp_solution(mixed), mixed)
+        assert verr > 0 and jump == 0.0
+        errs.append(verr)
+    assert errs[1] < 0.5 * errs[0]
+    mixed = _space("th-quad", 3, 2)
+    verr, _, _, _ = V.error_norms(np.zeros(mixed.ndof), mixed)
+    assert verr == pytest.approx(1.0, abs=1e-12)
+    mixed = _space("bdm", 3, 1)
+    x = np.random.default_rng(0).standard_normal(mixed.ndof)
+    _, p1, _, _ = V.error_norms(x, mixed)
+    shifted = x.copy()
+    shifted[mixed.offset:] += 7.5
+    _, p2, _, _ = V.error_norms(shifted, mixed)
+    assert p1 == pytest.approx(p2, rel=1e-10)
+
+
+# reference tests/test_bench.py:53-66
+def test_run_case_properties():
+    import paper_2409_14222_b200 as V
+    rec = V.run_case(V.RunSpec("th-tri", 2, nu=2, levels=1))
+    assert rec.converged and rec.err_h1_vel_rel < 0.05 and rec.max_div > 1e-3
+    rec = V.run_case(V.RunSpec("bdm", 2, nu=2, levels=2, rtol=1e-10))
+    assert rec.converged and rec.max_div <= 1e-8
+    rec = V.run_case(V.RunSpec("th-quad", 2, nu=2, levels=0, rtol=1e-10))
+    assert rec.converged and rec.iterations <= 2          # single level: exact preconditioner
+
+
+# reference tests/test_bench.py:79-102
+def test_sweep_deterministic_without_timings():
+    import paper_2409_14222_b200 as V
+    grid = [V.RunSpec("th-tri", 2, nu=nu, levels=lev, rtol=1e-8) for nu in (1, 2) for lev in (0, 1)]
+    outputs = []
+    for _ in range(2):
+        buf = io.StringIO()
+        records = V.sweep(grid, buf)
+        lines = buf.getvalue().strip().splitlines()
+        assert lines[0] == V.experiments.CSV_COLUMNS and len(lines) == 5 and len(records) == 4
+        rows = [line.split(",") for line in lines[1:]]
+        for row in rows:
+            row[11] = row[12] = "-"                       # wall-clock columns
+        outputs.append(rows)
+    assert outputs[0] == outputs[1]
+
+
+# reference tests/test_bench.py:115-160
+def test_stopping_plateau_and_cli(tmp_path):
+    import paper_2409_14222_b200 as V
+    from paper_2409_14222_b200.__main__ import main
+    rows = V.stopping_study("bdm", 1, 1, out=io.StringIO())
+    assert len(rows) == 1 and rows[0].resolved and 1e-15 < rows[0].required_rtol <= 1e-2
+    tight = V.run_case(V.RunSpec("bdm", 1, nu=1, levels=1, rtol=1e-12, max_it=200))
+    assert abs(rows[0].err_h1_vel_rel - tight.err_h1_vel_rel) <= 0.01 * tight.err_h1_vel_rel
+    out = tmp_path / "run.csv"
+    assert main(["run", "--case", "th-tri", "--k", "2", "--nu", "2", "--levels", "0", "--rtol",
+                 "1e-8", "--max-it", "50", "--out", str(out)]) == 0
+    lines = out.read_text().strip().splitlines()
+    assert lines[0] == V.experiments.CSV_COLUMNS and lines[1].startswith("th-tri,2,2,0,")
+    out = tmp_path / "stop.csv"
+    assert main(["stopping", "--case", "bdm", "--k", "1", "--max-levels", "1", "--out",
+                 str(out)]) == 0
+    lines = out.read_text().strip().splitlines()
+    assert len(lines) == 2 and lines[1].startswith("bdm,1,1,")
