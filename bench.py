@@ -552,6 +552,8 @@ class Level:
         old = mg.COARSE_CELLS_PER_SIDE
         mg.COARSE_CELLS_PER_SIDE = n0
         try:
+            import gc
+            gc.collect()                   # earlier configs' buffers are freed outside the timing
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             hier = V.build_hierarchy(case, k, refs, nu=2, damping=0.5)

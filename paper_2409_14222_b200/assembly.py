@@ -144,9 +144,22 @@ def interpolate(space: fem.Space, fn, *, boundary_only: bool = False) -> np.ndar
     coeffs = np.zeros(space.ndof)
     cells = np.flatnonzero(space.boundary_dof[space.cell_dofs].any(axis=1)) if boundary_only \
         else np.arange(topo.num_cells)
+    # point-evaluation elements (Lagrange: one point per functional): the
+    # per-DoF np.sum over one (scalar) or two (vector) products is a + (0. + b)
+    # — numpy copies the first term and adds the rest onto a zero-started
+    # partial sum, which matters only for the sign of zero — done for all the
+    # cell's DoFs at once
+    pointwise = el.mapping != "piola" and all(len(p) == 1 for p in el.dof_points)
+    if pointwise:
+        wmat = np.stack([np.asarray(w, dtype=float).reshape(-1) for w in el.dof_weights])
     for c in cells:
         verts = geom.vertex_coords[geom.cell_map_vertices[c]]
         fv = np.asarray(fn(fem.map_points(topo.cell_shape, verts, pts)), dtype=float)
+        if pointwise:
+            prod = wmat * fv.reshape(el.ndof, -1)
+            val = prod[:, 0] if prod.shape[1] == 1 else prod[:, 0] + (0.0 + prod[:, 1])
+            coeffs[space.cell_dofs[c]] = val / space.cell_dof_scale[c]
+            continue
         if el.mapping == "piola":
             _, det, inv = fem.cell_jacobians(topo.cell_shape, verts, pts)
             fv = det[:, None] * np.einsum("qab,qb->qa", inv, fv)
@@ -253,6 +266,29 @@ def _nnz(h):
 # prolongation (reference mg.py:91-167)
 # ----------------------------------------------------------------------------
 
+def _unique_rows(rows: np.ndarray):
+    """(index of the first occurrence of every distinct row, group id of every
+    row) like ``np.unique(rows, axis=0, return_index=True,
+    return_inverse=True)``, with the groups in ascending order of a 64-bit row
+    hash instead of lexicographic order (the callers only use first
+    occurrences).  The lexicographic sort of 5e5 ten-column rows was the
+    largest single item of the P2 256^2 setup (0.74 of 1.4 s); hashing the
+    rows and sorting one integer column is ~20x cheaper.  Every row is then
+    compared with its group's representative, so a hash collision cannot go
+    unnoticed (it falls back to the lexicographic path)."""
+    rows = np.ascontiguousarray(rows, dtype=np.float64) + 0.0        # -0.0 -> +0.0
+    mult = (np.arange(1, rows.shape[1] + 1, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)) \
+        | np.uint64(1)
+    h = (rows.view(np.uint64) * mult).sum(axis=1, dtype=np.uint64)
+    h ^= h >> np.uint64(29)
+    _, first, inv = np.unique(h, return_index=True, return_inverse=True)
+    inv = inv.ravel()
+    if not np.array_equal(rows, rows[first][inv]):
+        _, first, inv = np.unique(rows, axis=0, return_index=True, return_inverse=True)
+        inv = inv.ravel()
+    return first, inv
+
+
 def _configurations(coarse: fem.Space, fine: fem.Space, children):
     """Configuration id of every (parent, child) pair: the reference's cache
     key (coarse Jacobian, fine Jacobian, child origin in the parent's
@@ -270,7 +306,7 @@ def _configurations(coarse: fem.Space, fine: fem.Space, children):
     rel = np.linalg.solve(cj[par], (fxy[chi, 0] - cxy[par, 0])[..., None])[..., 0]
     keyrows = np.concatenate([cj[par].reshape(len(par), -1), fj[chi].reshape(len(par), -1),
                               rel.round(12)], axis=1)
-    _, first, inv = np.unique(keyrows, axis=0, return_index=True, return_inverse=True)
+    first, inv = _unique_rows(keyrows)
     order = np.argsort(first)                    # ids by first occurrence
     remap = np.empty_like(order)
     remap[order] = np.arange(len(order))

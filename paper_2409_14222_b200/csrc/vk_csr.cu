@@ -408,6 +408,19 @@ __global__ void csr_to_dense_kernel(int nrows, int ncols, const int* __restrict_
   }
 }
 
+// (col * nrows + row, value) of every stored entry, one thread per row
+__global__ void transpose_keys_kernel(int nrows, const int* __restrict__ ptr,
+                                      const int* __restrict__ col, const double* __restrict__ val,
+                                      unsigned long long* __restrict__ keys,
+                                      double* __restrict__ vals) {
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < nrows;
+       row += gridDim.x * blockDim.x)
+    for (int k = ptr[row]; k < ptr[row + 1]; ++k) {
+      keys[k] = (unsigned long long)col[k] * (unsigned long long)nrows + row;
+      vals[k] = val[k];
+    }
+}
+
 // greedy row blocks: <= kStreamNnz nonzeros and <= kStreamRows rows; a row
 // longer than kStreamNnz gets a block of its own
 std::vector<int32_t> make_row_blocks(const std::vector<int32_t>& p) {
@@ -492,29 +505,32 @@ extern "C" int vk_csr_create(const int32_t* indptr, const int32_t* indices, cons
 
 extern "C" int vk_csr_transpose(vk_csr_t a, vk_csr_t* out) {
   VK_REQUIRE(a && out, "vk_csr_transpose: null handle");
-  // Deterministic counting transpose: the entries of each output row come in
-  // ascending source-row order, i.e. the accumulation order of scipy's
-  // csc_matvec on masked.T (mg.py:44-45).  Setup-only; done on the host.
+  // Deterministic transpose on the device: entry (i, j) gets the key
+  // j * nrows + i and the keys are radix-sorted (vk_coo_to_csr), so the
+  // entries of each output row come in ascending source-row order — the
+  // accumulation order of scipy's csc_matvec on masked.T (mg.py:44-45).
+  // Every stored entry is kept (explicit zeros included: drop_abs < 0).
   const int64_t nnz = a->nnz;
-  std::vector<int32_t> p(a->nrows + 1), c(nnz);
-  std::vector<double> v(nnz);
-  VK_CHECK_CUDA(cudaMemcpy(p.data(), a->indptr, sizeof(int32_t) * (a->nrows + 1), cudaMemcpyDeviceToHost));
-  if (nnz) {
-    VK_CHECK_CUDA(cudaMemcpy(c.data(), a->indices, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
-    VK_CHECK_CUDA(cudaMemcpy(v.data(), a->data, sizeof(double) * nnz, cudaMemcpyDeviceToHost));
+  unsigned long long* keys = nullptr;
+  double* vals = nullptr;
+  cudaError_t e = cudaMalloc(&keys, sizeof(unsigned long long) * std::max<int64_t>(nnz, 1));
+  if (e == cudaSuccess) e = cudaMalloc(&vals, sizeof(double) * std::max<int64_t>(nnz, 1));
+  if (e == cudaSuccess && a->nrows > 0) {
+    transpose_keys_kernel<<<vk_grid(a->nrows, 256, 148 * 16), 256>>>(a->nrows, a->indptr,
+                                                                     a->indices, a->data, keys, vals);
+    e = cudaGetLastError();
   }
-  std::vector<int32_t> tp(a->ncols + 1, 0), tc(nnz);
-  std::vector<double> tv(nnz);
-  for (int64_t k = 0; k < nnz; ++k) tp[c[k] + 1]++;
-  for (int32_t j = 0; j < a->ncols; ++j) tp[j + 1] += tp[j];
-  std::vector<int32_t> cur(tp.begin(), tp.end() - 1);
-  for (int32_t i = 0; i < a->nrows; ++i)
-    for (int32_t k = p[i]; k < p[i + 1]; ++k) {
-      const int32_t dst = cur[c[k]]++;
-      tc[dst] = i;
-      tv[dst] = v[k];
-    }
-  return vk_csr_create(tp.data(), tc.data(), tv.data(), a->ncols, a->nrows, nnz, out);
+  int rc = VK_OK;
+  if (e != cudaSuccess) {
+    vk::set_error("vk_csr_transpose: %s", cudaGetErrorString(e));
+    rc = VK_ERR_CUDA;
+  } else {
+    rc = vk_coo_to_csr(nnz, reinterpret_cast<int64_t*>(keys), vals, a->ncols, a->nrows, 0, -1.0,
+                       nullptr, nullptr, nullptr, out);
+  }
+  cudaFree(keys);
+  cudaFree(vals);
+  return rc;
 }
 
 extern "C" int vk_csr_info(vk_csr_t a, int32_t* nrows, int32_t* ncols, int64_t* nnz) {
