@@ -220,3 +220,36 @@ def test_stopping_plateau_and_cli(tmp_path):
                  str(out)]) == 0
     lines = out.read_text().strip().splitlines()
     assert len(lines) == 2 and lines[1].startswith("bdm,1,1,")
+
+
+def _full_runs():
+    p = os.path.join(GOLDEN, "bench_full_golden.json")
+    return json.load(open(p))["runs"] if os.path.exists(p) else []
+
+
+@pytest.mark.parametrize("run", _full_runs(), ids=lambda r: f"{r['case']}_{r['k']}_{r['levels']}")
+def test_run_case_full_size_matches_reference(run, capsys):
+    """run_case at a BASELINE-size configuration (coarse 16^2 refined to 128^2,
+    reference-default Chebyshev bounds estimated on the device) against the
+    unmodified reference's record (tools/make_bench_full_golden.py)."""
+    import paper_2409_14222_b200 as V
+    from paper_2409_14222_b200 import mg
+    old = mg.COARSE_CELLS_PER_SIDE
+    mg.COARSE_CELLS_PER_SIDE = 16
+    try:
+        rec = V.run_case(V.RunSpec(run["case"], run["k"], nu=run["nu"], levels=run["levels"],
+                                   rtol=run["rtol"]))
+    finally:
+        mg.COARSE_CELLS_PER_SIDE = old
+    with capsys.disabled():
+        print(f"\n[{run['case']} k={run['k']} 128^2] device   {rec.csv_row()}\n"
+              f"{'':22s}reference {run['csv_row']}")
+    assert (rec.n_dofs, rec.m_dofs) == (run["n_dofs"], run["m_dofs"])
+    assert rec.converged == run["converged"]
+    assert abs(rec.iterations - run["iterations"]) <= 1
+    for key in ("err_h1_vel_rel", "err_l2_p_abs", "jump_seminorm"):
+        assert abs(getattr(rec, key) - run[key]) <= 1e-3 * abs(run[key]) + 1e-300, key
+    if run["case"] in ("bdm", "rt"):
+        assert rec.max_div <= 1e-8
+    else:
+        assert abs(rec.max_div - run["max_div"]) <= 1e-3 * run["max_div"]
