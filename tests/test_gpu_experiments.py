@@ -253,3 +253,25 @@ def test_run_case_full_size_matches_reference(run, capsys):
         assert rec.max_div <= 1e-8
     else:
         assert abs(rec.max_div - run["max_div"]) <= 1e-3 * run["max_div"]
+
+
+def _variant_runs():
+    p = os.path.join(GOLDEN, "bench_variants_golden.json")
+    return json.load(open(p)) if os.path.exists(p) else []
+
+
+@pytest.mark.parametrize("run", _variant_runs(), ids=lambda r: "-".join(
+    f"{k}={v}" for k, v in r["spec"].items() if k not in ("levels", "nu")))
+def test_run_case_non_default_fields(run, capsys):
+    """cheby = degree, weighting = unit, alpha, viscosity, seed, rtol / max_it:
+    every RunSpec field reaches the device path like the reference's."""
+    import paper_2409_14222_b200 as V
+    rec = V.run_case(V.RunSpec(**run["spec"]))
+    with capsys.disabled():
+        print(f"\ndevice    {rec.csv_row()}\nreference {run['csv_row']}")
+    assert (rec.n_dofs, rec.m_dofs, rec.converged) == (run["n_dofs"], run["m_dofs"],
+                                                       run["converged"])
+    assert abs(rec.iterations - run["iterations"]) <= 1
+    for key in ("err_h1_vel_rel", "err_l2_p_abs", "jump_seminorm"):
+        assert abs(getattr(rec, key) - run[key]) <= 1e-5 * abs(run[key]) + 1e-300, key
+    assert rec.csv_row().split(",")[:9] == run["csv_row"].split(",")[:9]
