@@ -650,11 +650,25 @@ static bool chunk_enabled() {
   return v;
 }
 
+// patch sets smaller than this take the split kernel (4 warps per patch,
+// plain loads); VK_SPLIT_MAX overrides it (A/B measurements).  Measured on
+// the captured V-cycles (tools/vcycle_time.py): with 2 * 1184 instead of
+// 4 * 1184 the 4225-patch levels of cfg2 / cfg4 move to the TMA kernels and
+// the V-cycle drops 1284 -> 1260 us (cfg2), 2469 -> 2447 us (cfg4); cfg3 and
+// cfg5 have no level in between and are unchanged bit for bit.
+static int split_max() {
+  static const int v = [] {
+    const char* e = getenv("VK_SPLIT_MAX");
+    return e ? atoi(e) : 148 * kApplyWarps * 2;
+  }();
+  return v;
+}
+
 // which K4a kernel a patch set runs (same decisions as vk_patches_solve)
 static const char* solve_kernel_name(const vk_patches_s* h) {
   const int rpl = (h->smax + 31) / 32;
   if (h->npatch == 0) return "none";
-  if (h->npatch < 148 * kApplyWarps * 4 && rpl <= 4) return "patch_solve_split_kernel";
+  if (h->npatch < split_max() && rpl <= 4) return "patch_solve_split_kernel";
   if (h->smax <= kBulkMaxS && !h->mixed_sizes && bulk_enabled() &&
       bulk_smem(h->smax) <= size_t(kBulkDynMax))
     return "patch_solve_bulk_kernel";
@@ -673,7 +687,7 @@ extern "C" int vk_patches_solve(vk_patches_t h, const double* r, double* zbuf, v
   const int rpl = (h->smax + 31) / 32;
   const int64_t bytes = 8 * h->inv_total + 20 * h->total;   // for the PDL decision
   cudaError_t le = cudaSuccess;
-  if (h->npatch > 0 && h->npatch < 148 * kApplyWarps * 4 && rpl <= 4) {
+  if (h->npatch > 0 && h->npatch < split_max() && rpl <= 4) {
     // coarse levels: 4 warps per patch
     constexpr int G = 4;
     const int grid = std::min((h->npatch + kApplyWarps / G - 1) / (kApplyWarps / G), 148 * 16);
