@@ -26,4 +26,31 @@ from .fem import build_mixed, strong_bc, structured_mesh
 from .experiments import (RunRecord, RunSpec, error_norms, expand_grid, run_case, stopping_study,
                           sweep)
 
+from .assembly import System as BlockSystem, manufactured_data
+from . import fem as _fem
+
+# host discretisation objects under the reference's public names
+# (stokesmg/__init__.py:15-35): same numbering, geometry and tabulations, bit
+# for bit (tests/test_fem.py)
+Mesh, MeshTopology, MeshGeometry = _fem.Mesh, _fem.Topology, _fem.Geometry
+FunctionSpace, MixedSpace, StrongBc = _fem.Space, _fem.Mixed, _fem.StrongBc
+QuadratureRule, ReferenceElement = _fem.Quadrature, _fem.Element
+build_space, make_quadrature = _fem.build_space, _fem.quadrature
+
+
+def build_structured_tri(n: int):
+    """Reference ``meshtopo.build_structured_tri`` (``meshtopo.py:177-205``)."""
+    return _fem.structured_mesh("tri", n)
+
+
+def build_structured_quad(n: int):
+    """Reference ``meshtopo.build_structured_quad`` (``meshtopo.py:208-231``)."""
+    return _fem.structured_mesh("quad", n)
+
+
+def tabulate(element, points):
+    """Reference ``elements.tabulate``: (values, gradients) on the reference cell."""
+    return element.tabulate(points)
+
+
 __version__ = "0.1.0"

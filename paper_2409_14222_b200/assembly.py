@@ -124,6 +124,44 @@ def facet_tables(vel: fem.Space):
     return info, geo, erule, tabs_v, tabs_g
 
 
+class ManufacturedSolution:
+    """Closed-form enclosed-flow solution with zero pressure (reference
+    ``assembly.ManufacturedSolution``, ``assembly.py:54-87``): u = (sin pi x
+    cos pi y, -cos pi x sin pi y), divergence-free with zero normal component
+    on the unit-square boundary; forcing 2 pi^2 nu u.  Host evaluation for
+    callers; the device kernels evaluate the same formulas per quadrature
+    point (``vk_assemble_load``, ``vk_error_cells``)."""
+
+    def __init__(self, viscosity: float = 1.0):
+        self.viscosity = viscosity
+
+    @staticmethod
+    def velocity(pts):
+        return manufactured_velocity(np.asarray(pts, dtype=float))
+
+    @staticmethod
+    def velocity_gradient(pts):
+        pts = np.asarray(pts, dtype=float)
+        sx, cx = np.sin(np.pi * pts[:, 0]), np.cos(np.pi * pts[:, 0])
+        sy, cy = np.sin(np.pi * pts[:, 1]), np.cos(np.pi * pts[:, 1])
+        g = np.empty((len(pts), 2, 2))
+        g[:, 0, 0], g[:, 0, 1] = np.pi * cx * cy, -np.pi * sx * sy
+        g[:, 1, 0], g[:, 1, 1] = np.pi * sx * sy, -np.pi * cx * cy
+        return g
+
+    @staticmethod
+    def pressure(pts):
+        return np.zeros(len(pts))
+
+    def forcing(self, pts):
+        return 2.0 * np.pi ** 2 * self.viscosity * self.velocity(pts)
+
+
+def manufactured_data(viscosity: float = 1.0) -> ManufacturedSolution:
+    """Reference ``assembly.manufactured_data`` (``assembly.py:90-91``)."""
+    return ManufacturedSolution(viscosity)
+
+
 def manufactured_velocity(pts):
     """Reference ``ManufacturedSolution.velocity`` (``assembly.py:65-69``)."""
     x, y = pts[:, 0], pts[:, 1]

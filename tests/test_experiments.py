@@ -96,3 +96,41 @@ def test_cli_parses_reference_flags():
                 "stopping --case th-tri --k 2 --max-levels 1 --out s.csv", "sweep --out s.csv"):
         with pytest.raises(SystemExit):
             p.parse_args(bad.split())
+
+
+def test_reference_public_names_and_manufactured_data():
+    """Top-level names of the reference package (stokesmg/__init__.py:15-35)
+    that the drop-in mirrors, and the manufactured solution's properties
+    (reference tests/test_assembly.py:31-66)."""
+    import numpy as np
+    import paper_2409_14222_b200 as V
+    for name in ("BlockSystem", "ProblemConfig", "assemble", "manufactured_data", "RunRecord",
+                 "RunSpec", "error_norms", "run_case", "stopping_study", "sweep", "QuadratureRule",
+                 "ReferenceElement", "make_quadrature", "tabulate", "EntityRef", "Mesh",
+                 "MeshGeometry", "MeshTopology", "build_structured_quad", "build_structured_tri",
+                 "ChebyshevParams", "MgHierarchy", "TransferPair", "build_hierarchy",
+                 "build_prolongation", "chebyshev_relax", "make_preconditioner", "v_cycle",
+                 "FunctionSpace", "MixedSpace", "StrongBc", "build_mixed", "build_space",
+                 "interpolate", "strong_bc", "DenseFactorization", "KrylovReport",
+                 "SingularMatrixError", "estimate_lambda_max", "extract_submatrix", "fgmres",
+                 "lu_factor", "lu_solve", "nullspace_projector", "spmv", "triple_product", "Patch",
+                 "PatchSet", "apply_additive", "build_patches_hdiv_extended",
+                 "build_patches_taylor_hood", "factor_patches"):
+        assert hasattr(V, name), name
+    mesh = V.build_structured_tri(3)
+    assert mesh.topology.num_cells == 18 and V.build_structured_quad(3).topology.num_cells == 9
+    assert abs(V.make_quadrature("tri", 4).weights.sum() - 0.5) < 1e-15
+    data = V.manufactured_data()
+    pts = np.random.default_rng(0).random((50, 2))
+    g = data.velocity_gradient(pts)
+    assert np.allclose(g[:, 0, 0] + g[:, 1, 1], 0.0, atol=1e-14)          # divergence free
+    assert np.allclose(0.5 * (g[:, 0, 1] + g[:, 1, 0]), 0.0, atol=1e-14)  # no shear strain
+    assert np.allclose(data.velocity(np.array([[0.5, 0.0]])), [[1.0, 0.0]])
+    assert np.allclose(V.manufactured_data(3.0).forcing(pts), 3 * data.forcing(pts))
+    assert np.allclose(data.forcing(pts), 2 * np.pi ** 2 * data.velocity(pts))
+    h = 1e-6
+    for d in range(2):
+        e = np.zeros(2)
+        e[d] = h
+        fd = (data.velocity(pts + e) - data.velocity(pts - e)) / (2 * h)
+        assert np.allclose(g[:, :, d], fd, atol=1e-8)
