@@ -531,7 +531,7 @@ class Level:
         t_c = time.perf_counter() - t0
         n0 = c.A.shape[0]
         del inv
-        return {"kernel": "K3 factor_tile_kernel (extraction + guard + Gauss-Jordan inverse)",
+        return {"kernel": "K2 extract_blocks_kernel + K3 factor_warp / factor_rows / factor_blk kernels (guard + Gauss-Jordan inverse), re-factorisation of every patch",
                 "ms": ms, "lu_equiv_gflop": flops / 1e9,
                 "tflops_lu_equiv": flops / (ms * 1e-3) / 1e12,
                 "fp64_peak_tflops": FP64_PEAK_TFLOPS,
