@@ -939,11 +939,15 @@ __host__ __device__ constexpr size_t blk_smem_bytes() {
          sizeof(int) * (4 * size_t(S));
 }
 
+#ifndef VK_BLK_THREADS
+#define VK_BLK_THREADS 256      // threads of factor_blk_kernel (a multiple of 32)
+#endif
+
 template <int S>
-__global__ void __launch_bounds__(256, 1) factor_blk_kernel(
+__global__ void __launch_bounds__(VK_BLK_THREADS, 1) factor_blk_kernel(
     const int* __restrict__ plist, int count, const int64_t* __restrict__ off,
     const int64_t* __restrict__ opoff, double* __restrict__ inv, int* __restrict__ status) {
-  constexpr int NT = 256, NW = NT / 32, LD = S + 1, NB = 8, TT = S / 8, R = (S + 31) / 32;
+  constexpr int NT = VK_BLK_THREADS, NW = NT / 32, LD = S + 1, NB = 8, TT = S / 8, R = (S + 31) / 32;
   constexpr int NONE = 0x7fffffff;
   static_assert(S % 8 == 0, "8x8 tiles");
   extern __shared__ __align__(16) double smem[];
@@ -1069,13 +1073,13 @@ __global__ void __launch_bounds__(256, 1) factor_blk_kernel(
         // warps 1..7: every other column tile except panels pp and pp+1
 #ifndef VK_BLK_NOUPD
 #ifndef VK_BLK_ALL_WARPS
-        // warp 4 shares warp 0's scheduler (warp id mod 4) and sits this phase
-        // out: the panel chain, which bounds the class, gets the issue slots of
+        // the warps that share warp 0's scheduler (warp id mod 4 == 0) sit this
+        // phase out: the panel chain, which bounds the class, gets the issue slots of
         // its SMSP to itself while six warps on the other three SMSPs update
         // (same units, same results; measured: 128-class 12.98 -> 11.87 ms,
         // 104-class 9.06 -> 8.45 ms)
-        if (warp != 4)
-          blk_update<S>(W, Pb, Rb, isp, pp, ahead, warp < 4 ? warp - 1 : warp - 2, NW - 2, lane);
+        if (warp & 3)
+          blk_update<S>(W, Pb, Rb, isp, pp, ahead, warp - 1 - (warp >> 2), NW - (NW + 3) / 4, lane);
 #else
         blk_update<S>(W, Pb, Rb, isp, pp, ahead, warp - 1, NW - 1, lane);
 #endif
@@ -2041,9 +2045,10 @@ int launch_class(int smax, const int* d_ids, int count, const vk_patches_s* h, c
     auto kern = factor_blk_kernel<S_>;                                                          \
     const size_t dsm = blk_smem_bytes<S_>();                                                    \
     e = vk_smem_optin((const void*)kern, int(dsm));                                             \
-    const int grid = std::max(1, std::min(count, vk_resident_blocks((const void*)kern, 256, dsm))); \
+    const int grid = std::max(1, std::min(count, vk_resident_blocks((const void*)kern,          \
+                                                                    VK_BLK_THREADS, dsm)));     \
     if (e == cudaSuccess)                                                                       \
-      kern<<<grid, 256, dsm, st>>>(d_ids, count, h->off, h->opoff, h->inv, d_status);          \
+      kern<<<grid, VK_BLK_THREADS, dsm, st>>>(d_ids, count, h->off, h->opoff, h->inv, d_status); \
   } while (0)
     if (smax <= 80) VK_BLK(80);
     else if (smax <= 96) VK_BLK(96);
